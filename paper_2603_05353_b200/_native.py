@@ -1,0 +1,94 @@
+"""ctypes binding of the sm_100a native library (C ABI in include/ifkv.h).
+
+There is no fallback: if ``_build/libifkv.so`` is missing or no CUDA device
+is present, every compute entry point raises NativeError.  Status codes map
+to the package's exceptions: IFKV_ERR_ARG -> ConfigurationError,
+IFKV_ERR_CUDA -> NativeError, each with the library's thread-local message.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+from .errors import ConfigurationError, NativeError
+
+LIB_PATH = Path(__file__).resolve().parent / "_build" / "libifkv.so"
+
+IFKV_F32, IFKV_BF16 = 0, 1
+OUT_F32, OUT_BF16, OUT_SPLIT3 = 0, 1, 2
+AGG_NONE, AGG_SUM, AGG_MEAN, AGG_MAX = -1, 0, 1, 2
+AGG_CODES = {"sum": AGG_SUM, "mean": AGG_MEAN, "max": AGG_MAX}
+
+P, I32, I64, F32, F64 = C.c_void_p, C.c_int, C.c_int64, C.c_float, C.c_double
+
+# name -> argtypes (restype is always c_int status unless noted)
+SIGNATURES = {
+    "ifkv_rope_table": [P, I32, I32, F64, P, P],
+    "ifkv_rotate_rows": [I32, P, P, I64, I32, I32, I32, I32, P, P, P],
+    "ifkv_assemble_gather": [I32, I32, P, P, P, P, P, P, P, I64, I32, I32, P],
+    "ifkv_add_rmsnorm": [P, P, I32, I32, P, I32, I32, I32, P, P],
+    "ifkv_silu_mul": [P, I32, I32, I32, I32, I32, P, P],
+    "ifkv_embed_rows": [P, I32, P, I32, I32, P, P],
+    "ifkv_split3": [P, I64, P, P],
+    "ifkv_qkv_rope_scatter": [P, I32, I32, I32, I32, I32, I32, P, I32, P, P, P, P, P],
+    "ifkv_prompt_attn_partial": [I32, P, P, P, P, P, P, I32, I32, I32, I32, I32, F32, P, P, P],
+    "ifkv_prompt_attn_merge": [P, P, P, I32, I32, I32, I32, P, P, P],
+    "ifkv_score_columns": [I32, P, P, P, I32, P, I32, I32, I32, I32, F32, P, P],
+    "ifkv_rotate_queries": [P, I32, I32, I32, I32, P, P, I32, P, P, P],
+    "ifkv_topk_segments": [P, P, P, P, I32, P, I32, P, P],
+    "ifkv_recompute_attn": [I32, P, P, P, P, I32, I32, I32, I32, F32, P, P],
+    "ifkv_recompute_attn_simt": [I32, P, P, P, P, I32, I32, I32, I32, F32, P, P],
+    "ifkv_recompute_attn_tc_supported": [I32, I32, I32, I32],
+}
+EXPORTS = tuple(SIGNATURES) + ("ifkv_last_error", "ifkv_abi_version")
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load(path: Path = LIB_PATH):
+    """Load (once) and type the library; raise NativeError if it is absent."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not path.exists():
+            raise NativeError(
+                f"native library {path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        lib = C.CDLL(str(path))
+        for name, args in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = C.c_int
+        lib.ifkv_last_error.argtypes = []
+        lib.ifkv_last_error.restype = C.c_char_p
+        lib.ifkv_abi_version.argtypes = []
+        lib.ifkv_abi_version.restype = C.c_int
+        _lib = lib
+        return lib
+
+
+def call(name: str, *args) -> int:
+    """Invoke an entry point and translate its status code."""
+    lib = load()
+    status = getattr(lib, name)(*args)
+    if status == 0 or name.endswith("_supported"):
+        return status
+    msg = lib.ifkv_last_error().decode(errors="replace")
+    if status == 2:
+        raise ConfigurationError(f"{name}: {msg}")
+    raise NativeError(f"{name}: {msg}")
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a torch tensor (None -> NULL)."""
+    return None if t is None else t.data_ptr()
+
+
+def stream_handle() -> int:
+    import torch
+
+    return torch.cuda.current_stream().cuda_stream

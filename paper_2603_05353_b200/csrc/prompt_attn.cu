@@ -1,0 +1,241 @@
+// Prompt attention over an injected KV prefix, split into <=128-key work
+// items (flash-decoding style), plus the capture-layer column scorer.
+// Generic SIMT fp32 path: any even Dh <= 256, any GQA ratio, fp32 or bf16
+// K/V.  Arithmetic is fp32 throughout (fp32-accurate scoring, SURVEY §7 hard
+// part 1); reference: selection.py:127-169, model.py:297-315, 352-360.
+#include "common.cuh"
+
+namespace ifkv {
+
+constexpr int kItemKeysMax = 128;
+
+// K/V element of the item's key j (kv head g), as fp32.
+__device__ __forceinline__ const void* item_kv_base(const ifkv_attn_item& it, int kv_dtype, const void* slab,
+                                                    const float* prompt, int M, int Hkv, int Dh, int g, int j,
+                                                    bool& is_f32, int64_t& idx) {
+  if (it.prompt) {
+    is_f32 = true;
+    idx = (((int64_t)it.group * M + it.key_row0 + j) * Hkv + g) * Dh;
+    return prompt;
+  }
+  is_f32 = kv_dtype == IFKV_F32;
+  idx = ((int64_t)(it.key_row0 + j) * Hkv + g) * Dh;
+  return slab;
+}
+
+// Stage the item's keys (and values) of kv head g into shared memory as fp32.
+// Ks has row stride Dh + 1 (conflict-free per-key dot products).
+__device__ void stage_item(const ifkv_attn_item& it, int kv_dtype, const void* k_slab, const void* v_slab,
+                           const float* k_prompt, const float* v_prompt, int M, int Hkv, int Dh, int g, float* Ks,
+                           float* Vs) {
+  const int n = it.n_keys;
+  for (int t = threadIdx.x; t < n * Dh; t += blockDim.x) {
+    int j = t / Dh, d = t - j * Dh;
+    bool f32;
+    int64_t idx;
+    const void* kb = item_kv_base(it, kv_dtype, k_slab, k_prompt, M, Hkv, Dh, g, j, f32, idx);
+    Ks[j * (Dh + 1) + d] = f32 ? reinterpret_cast<const float*>(kb)[idx + d] : load_as_f32(kb, IFKV_BF16, idx + d);
+    if (Vs) {
+      const void* vb = item_kv_base(it, kv_dtype, v_slab, v_prompt, M, Hkv, Dh, g, j, f32, idx);
+      Vs[j * Dh + d] = f32 ? reinterpret_cast<const float*>(vb)[idx + d] : load_as_f32(vb, IFKV_BF16, idx + d);
+    }
+  }
+}
+
+// grid (n_items, Hkv), 256 threads.  Warp w handles query rows w, w+8, ...
+// of the item's group restricted to kv head g (grp heads x M rows).
+__global__ void __launch_bounds__(256) prompt_attn_partial_kernel(
+    int kv_dtype, const float* __restrict__ qd, const void* __restrict__ k_slab, const void* __restrict__ v_slab,
+    const float* __restrict__ k_prompt, const float* __restrict__ v_prompt, const ifkv_attn_item* __restrict__ items,
+    int H, int Hkv, int M, int Dh, float scale, float* __restrict__ part_ml, float* __restrict__ part_o) {
+  extern __shared__ float smem[];
+  const ifkv_attn_item it = items[blockIdx.x];
+  const int g = blockIdx.y;
+  const int grp = H / Hkv;
+  const int n = it.n_keys;
+  float* Ks = smem;                                  // [n][Dh+1]
+  float* Vs = Ks + kItemKeysMax * (Dh + 1);           // [n][Dh]
+  float* Qs = Vs + kItemKeysMax * Dh;                 // [8][Dh]
+  stage_item(it, kv_dtype, k_slab, v_slab, k_prompt, v_prompt, M, Hkv, Dh, g, Ks, Vs);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* q = Qs + warp * Dh;
+  const int rows = grp * M;
+  for (int r = warp; r < rows; r += 8) {
+    const int h = g * grp + r / M, m = r % M;
+    const float* qsrc = qd + (((int64_t)it.qset * H + h) * M + m) * Dh;
+    for (int d = lane; d < Dh; d += 32) q[d] = qsrc[d];
+    __syncwarp();
+    float logit[4];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      int j = lane + 32 * t;
+      logit[t] = -INFINITY;
+      if (j < n && (!it.prompt || it.key_row0 + j <= m)) {
+        const float* kr = Ks + j * (Dh + 1);
+        float acc = 0.f;
+        for (int d = 0; d < Dh; ++d) acc = fmaf(q[d], kr[d], acc);
+        logit[t] = acc * scale;
+      }
+      mx = fmaxf(mx, logit[t]);
+    }
+    mx = warp_max(mx);
+    float p[4], l = 0.f;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      p[t] = logit[t] == -INFINITY ? 0.f : expf(logit[t] - mx);
+      l += p[t];
+    }
+    l = warp_sum(l);
+    float o[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) o[u] = 0.f;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (32 * t >= n) break;
+      for (int jj = 0; jj < 32; ++jj) {
+        float pj = __shfl_sync(0xffffffffu, p[t], jj);
+        int j = 32 * t + jj;
+        if (j >= n) break;
+        const float* vr = Vs + j * Dh;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          int d = lane + 32 * u;
+          if (d < Dh) o[u] = fmaf(pj, vr[d], o[u]);
+        }
+      }
+    }
+    const int64_t row_id = ((int64_t)blockIdx.x * H + h) * M + m;
+    if (lane == 0) {
+      part_ml[2 * row_id] = mx;
+      part_ml[2 * row_id + 1] = l;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      int d = lane + 32 * u;
+      if (d < Dh) part_o[row_id * Dh + d] = o[u];
+    }
+    __syncwarp();
+  }
+}
+
+// grid (G * H * M), Dh threads (<= 256): merge the group's items in order.
+__global__ void prompt_attn_merge_kernel(const float* __restrict__ part_ml, const float* __restrict__ part_o,
+                                         const int32_t* __restrict__ item_begin, int H, int M, int Dh,
+                                         float* __restrict__ ctx, float* __restrict__ ml) {
+  const int r = blockIdx.x;  // (g, h, m)
+  const int m = r % M, h = (r / M) % H, g = r / (M * H);
+  const int b = item_begin[g], e = item_begin[g + 1];
+  float mx = -INFINITY;
+  for (int i = b; i < e; ++i) {
+    float mi = part_ml[2 * (((int64_t)i * H + h) * M + m)];
+    mx = fmaxf(mx, mi);
+  }
+  float l = 0.f, o = 0.f;
+  const int d = threadIdx.x;
+  for (int i = b; i < e; ++i) {
+    int64_t row = ((int64_t)i * H + h) * M + m;
+    float mi = part_ml[2 * row];
+    if (mi == -INFINITY) continue;
+    float a = expf(mi - mx);
+    l += part_ml[2 * row + 1] * a;
+    if (d < Dh) o += part_o[row * Dh + d] * a;
+  }
+  if (d < Dh) ctx[(((int64_t)g * M + m) * H + h) * Dh + d] = o / l;
+  if (d == 0) {
+    ml[2 * (((int64_t)g * H + h) * M + m)] = mx;
+    ml[2 * (((int64_t)g * H + h) * M + m) + 1] = l;
+  }
+}
+
+// grid (n_items), 128 threads: thread j owns key column j of the item and
+// sums p over all heads and prompt rows in a fixed order (deterministic).
+__global__ void __launch_bounds__(128) score_columns_kernel(int kv_dtype, const float* __restrict__ qd,
+                                                            const void* __restrict__ k_slab,
+                                                            const ifkv_attn_item* __restrict__ items,
+                                                            const float* __restrict__ ml, int H, int Hkv, int M,
+                                                            int Dh, float scale, float* __restrict__ scores) {
+  extern __shared__ float smem[];
+  const ifkv_attn_item it = items[blockIdx.x];
+  if (!it.score || it.prompt) return;
+  float* Ks = smem;                          // [n][Dh+1]
+  float* Qs = Ks + kItemKeysMax * (Dh + 1);  // [M][Dh] for one head
+  const int grp = H / Hkv;
+  const int j = threadIdx.x;
+  float colsum = 0.f;
+  for (int g = 0; g < Hkv; ++g) {
+    __syncthreads();
+    stage_item(it, kv_dtype, k_slab, nullptr, nullptr, nullptr, M, Hkv, Dh, g, Ks, nullptr);
+    for (int hh = 0; hh < grp; ++hh) {
+      const int h = g * grp + hh;
+      __syncthreads();
+      const float* qsrc = qd + ((int64_t)it.qset * H + h) * M * Dh;
+      for (int t = threadIdx.x; t < M * Dh; t += blockDim.x) Qs[t] = qsrc[t];
+      __syncthreads();
+      if (j < it.n_keys) {
+        const float* kr = Ks + j * (Dh + 1);
+        for (int m = 0; m < M; ++m) {
+          const float* q = Qs + m * Dh;
+          float acc = 0.f;
+          for (int d = 0; d < Dh; ++d) acc = fmaf(q[d], kr[d], acc);
+          int64_t s = 2 * (((int64_t)it.group * H + h) * M + m);
+          colsum += expf(acc * scale - ml[s]) / ml[s + 1];
+        }
+      }
+    }
+  }
+  if (j < it.n_keys) scores[it.key_row0 + j] = colsum / (float)H;
+}
+
+}  // namespace ifkv
+
+using namespace ifkv;
+
+static size_t partial_smem(int Dh) { return (size_t)(kItemKeysMax * (Dh + 1) + kItemKeysMax * Dh + 8 * Dh) * 4; }
+static size_t score_smem(int Dh, int M) { return (size_t)(kItemKeysMax * (Dh + 1) + M * Dh) * 4; }
+
+extern "C" int ifkv_prompt_attn_partial(int kv_dtype, const float* qd, const void* k_slab, const void* v_slab,
+                                        const float* k_prompt, const float* v_prompt, const ifkv_attn_item* items,
+                                        int n_items, int H, int Hkv, int M, int Dh, float scale, float* part_ml,
+                                        float* part_o, void* stream) {
+  IFKV_CHECK_ARG(kv_dtype == IFKV_F32 || kv_dtype == IFKV_BF16, "prompt_attn_partial: bad dtype");
+  IFKV_CHECK_ARG(Dh % 2 == 0 && Dh <= 256 && H % Hkv == 0 && M > 0, "prompt_attn_partial: bad shape");
+  if (n_items <= 0) return IFKV_OK;
+  size_t sm = partial_smem(Dh);
+  IFKV_CUDA_CALL(cudaFuncSetAttribute(prompt_attn_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sm),
+                 "prompt_attn_partial: smem attribute");
+  dim3 grid(n_items, Hkv);
+  prompt_attn_partial_kernel<<<grid, 256, sm, as_stream(stream)>>>(kv_dtype, qd, k_slab, v_slab, k_prompt,
+                                                                     v_prompt, items, H, Hkv, M, Dh, scale, part_ml,
+                                                                     part_o);
+  IFKV_LAUNCH_CHECK("prompt_attn_partial");
+  return IFKV_OK;
+}
+
+extern "C" int ifkv_prompt_attn_merge(const float* part_ml, const float* part_o, const int32_t* item_begin, int G,
+                                      int H, int M, int Dh, float* ctx, float* ml, void* stream) {
+  IFKV_CHECK_ARG(Dh <= 256 && G > 0, "prompt_attn_merge: bad shape");
+  int threads = ((Dh + 31) / 32) * 32;
+  prompt_attn_merge_kernel<<<G * H * M, threads, 0, as_stream(stream)>>>(part_ml, part_o, item_begin, H, M, Dh, ctx,
+                                                                          ml);
+  IFKV_LAUNCH_CHECK("prompt_attn_merge");
+  return IFKV_OK;
+}
+
+extern "C" int ifkv_score_columns(int kv_dtype, const float* qd, const void* k_slab, const ifkv_attn_item* items,
+                                  int n_items, const float* ml, int H, int Hkv, int M, int Dh, float scale,
+                                  float* scores, void* stream) {
+  IFKV_CHECK_ARG(kv_dtype == IFKV_F32 || kv_dtype == IFKV_BF16, "score_columns: bad dtype");
+  IFKV_CHECK_ARG(Dh % 2 == 0 && Dh <= 256 && H % Hkv == 0, "score_columns: bad shape");
+  if (n_items <= 0) return IFKV_OK;
+  size_t sm = score_smem(Dh, M);
+  IFKV_CHECK_ARG(sm <= 220 * 1024, "score_columns: M*Dh too large for shared memory");
+  IFKV_CUDA_CALL(cudaFuncSetAttribute(score_columns_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
+                 "score_columns: smem attribute");
+  score_columns_kernel<<<n_items, 128, sm, as_stream(stream)>>>(kv_dtype, qd, k_slab, items, ml, H, Hkv, M, Dh,
+                                                                 scale, scores);
+  IFKV_LAUNCH_CHECK("score_columns");
+  return IFKV_OK;
+}

@@ -1,0 +1,133 @@
+// Selective-recompute attention, generic SIMT path (fp32 mode, any even
+// Dh <= 256, any GQA ratio).  Query row i attends keys 0..horizon[i]
+// (recompute.py:92-93, 114; masked_attention model.py:297-315) with an
+// online fp32 softmax.  The bf16 / Dh=128 hot path is the tcgen05 kernel in
+// tc_recompute_attn.cu; this kernel is its numerical cross-check.
+#include "common.cuh"
+
+namespace ifkv {
+
+constexpr int kRaTokens = 16;  // query rows (tokens) per CTA, one head
+constexpr int kRaKeys = 32;    // keys per smem block
+
+template <typename T>
+__global__ void __launch_bounds__(128) recompute_attn_simt_kernel(const T* __restrict__ q, const T* __restrict__ k,
+                                                                  const T* __restrict__ v,
+                                                                  const int64_t* __restrict__ horizon, int S, int H,
+                                                                  int Hkv, int Dh, float scale, T* __restrict__ out) {
+  extern __shared__ float smem[];
+  float* Ks = smem;                          // [32][Dh+1]
+  float* Vs = Ks + kRaKeys * (Dh + 1);       // [32][Dh]
+  float* Qs = Vs + kRaKeys * Dh;             // [16][Dh]
+  const int t0 = blockIdx.x * kRaTokens;
+  const int h = blockIdx.y;
+  const int g = h / (H / Hkv);
+  const int nt = min(kRaTokens, S - t0);
+  for (int t = threadIdx.x; t < nt * Dh; t += blockDim.x) {
+    int r = t / Dh, d = t - r * Dh;
+    Qs[t] = to_f32(q[((int64_t)(t0 + r) * H + h) * Dh + d]);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int64_t hz[4];
+  float m[4], l[4], o[4][8];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    int row = warp * 4 + r;
+    hz[r] = row < nt ? horizon[t0 + row] : -1;
+    m[r] = -INFINITY;
+    l[r] = 0.f;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) o[r][u] = 0.f;
+  }
+  const int64_t kmax = horizon[t0 + nt - 1];
+  for (int64_t k0 = 0; k0 <= kmax; k0 += kRaKeys) {
+    __syncthreads();
+    const int nk = (int)(kmax + 1 - k0 < kRaKeys ? kmax + 1 - k0 : kRaKeys);
+    for (int t = threadIdx.x; t < nk * Dh; t += blockDim.x) {
+      int j = t / Dh, d = t - j * Dh;
+      int64_t src = ((k0 + j) * Hkv + g) * Dh + d;
+      Ks[j * (Dh + 1) + d] = to_f32(k[src]);
+      Vs[j * Dh + d] = to_f32(v[src]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      if (hz[r] < k0) continue;  // warp-uniform
+      const float* qr = Qs + (warp * 4 + r) * Dh;
+      float s = -INFINITY;
+      if (lane < nk && k0 + lane <= hz[r]) {
+        const float* kr = Ks + lane * (Dh + 1);
+        float acc = 0.f;
+        for (int d = 0; d < Dh; ++d) acc = fmaf(qr[d], kr[d], acc);
+        s = acc * scale;
+      }
+      float mb = warp_max(s);
+      float mn = fmaxf(m[r], mb);
+      float p = s == -INFINITY ? 0.f : expf(s - mn);
+      float alpha = m[r] == -INFINITY ? 0.f : expf(m[r] - mn);
+      l[r] = l[r] * alpha + warp_sum(p);
+      m[r] = mn;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) o[r][u] *= alpha;
+      for (int j = 0; j < nk; ++j) {
+        float pj = __shfl_sync(0xffffffffu, p, j);
+        const float* vr = Vs + j * Dh;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          int d = lane + 32 * u;
+          if (d < Dh) o[r][u] = fmaf(pj, vr[d], o[r][u]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    int row = warp * 4 + r;
+    if (row >= nt) continue;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      int d = lane + 32 * u;
+      if (d < Dh) out[((int64_t)(t0 + row) * H + h) * Dh + d] = from_f32<T>(o[r][u] / l[r]);
+    }
+  }
+}
+
+}  // namespace ifkv
+
+using namespace ifkv;
+
+extern "C" int ifkv_recompute_attn_tc(const void* q, const void* k_layer, const void* v_layer, const int64_t* horizon,
+                                      int S, int H, int Hkv, int Dh, float scale, void* out, void* stream);
+extern "C" int ifkv_recompute_attn_tc_supported(int dtype, int H, int Hkv, int Dh);
+
+extern "C" int ifkv_recompute_attn_simt(int dtype, const void* q, const void* k_layer, const void* v_layer,
+                                        const int64_t* horizon, int S, int H, int Hkv, int Dh, float scale, void* out,
+                                        void* stream) {
+  IFKV_CHECK_ARG(dtype == IFKV_F32 || dtype == IFKV_BF16, "recompute_attn: bad dtype");
+  IFKV_CHECK_ARG(Dh % 2 == 0 && Dh <= 256 && Hkv > 0 && H % Hkv == 0, "recompute_attn: bad shape");
+  if (S <= 0) return IFKV_OK;
+  size_t sm = (size_t)(kRaKeys * (Dh + 1) + kRaKeys * Dh + kRaTokens * Dh) * 4;
+  dim3 grid((S + kRaTokens - 1) / kRaTokens, H);
+  if (dtype == IFKV_BF16) {
+    auto kern = recompute_attn_simt_kernel<__nv_bfloat16>;
+    IFKV_CUDA_CALL(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "recompute_attn");
+    kern<<<grid, 128, sm, as_stream(stream)>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k_layer,
+                                               (const __nv_bfloat16*)v_layer, horizon, S, H, Hkv, Dh, scale,
+                                               (__nv_bfloat16*)out);
+  } else {
+    auto kern = recompute_attn_simt_kernel<float>;
+    IFKV_CUDA_CALL(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "recompute_attn");
+    kern<<<grid, 128, sm, as_stream(stream)>>>((const float*)q, (const float*)k_layer, (const float*)v_layer, horizon,
+                                               S, H, Hkv, Dh, scale, (float*)out);
+  }
+  IFKV_LAUNCH_CHECK("recompute_attn_simt");
+  return IFKV_OK;
+}
+
+extern "C" int ifkv_recompute_attn(int dtype, const void* q, const void* k_layer, const void* v_layer,
+                                   const int64_t* horizon, int S, int H, int Hkv, int Dh, float scale, void* out,
+                                   void* stream) {
+  if (ifkv_recompute_attn_tc_supported(dtype, H, Hkv, Dh))
+    return ifkv_recompute_attn_tc(q, k_layer, v_layer, horizon, S, H, Hkv, Dh, scale, out, stream);
+  return ifkv_recompute_attn_simt(dtype, q, k_layer, v_layer, horizon, S, H, Hkv, Dh, scale, out, stream);
+}

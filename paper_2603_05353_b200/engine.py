@@ -1,0 +1,383 @@
+"""Device engine: typed wrappers over the C ABI plus the two layer loops the
+path is built from.
+
+* ``prompt_forward`` -- M prompt rows (one or many query groups) run forward
+  on top of an injected, per-row-rotated KV prefix, fp32-accurate end to end
+  (selection.py:127-169 via model.py:379-462).  bf16 weights are exact
+  tensor-core operands; fp32 activations enter GEMMs as three bf16 terms
+  (hi + mid + lo) whose fp32 products are summed, so the prompt forward is
+  fp32-accurate and the selected set matches the float64 reference.
+* ``layer_stack`` -- S tokens advance through every layer, their fresh K/V
+  scattered into a slab in place before the layer's attention reads it
+  (recompute.py:67-122; the same loop prefills chunks, cache.py:74-99).
+
+PyTorch is plumbing here: tensors own HBM, the current stream orders work,
+cuBLAS (torch.mm) runs the plain projection GEMMs.  Everything else is an
+sm_100a kernel behind include/ifkv.h.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _native as N
+from .errors import ConfigurationError
+
+ITEM_KEYS = 128  # keys per prompt-attention work item (<= kItemKeysMax)
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def dt_code(t) -> int:
+    torch = _torch()
+    if t.dtype == torch.bfloat16:
+        return N.IFKV_BF16
+    if t.dtype == torch.float32:
+        return N.IFKV_F32
+    raise ConfigurationError(f"unsupported tensor dtype {t.dtype}")
+
+
+def _s():
+    return N.stream_handle()
+
+
+def require_cuda(t, what: str):
+    if not t.is_cuda:
+        raise ConfigurationError(f"{what} must be a CUDA tensor")
+
+
+# ---------------------------------------------------------------------------
+# thin wrappers
+# ---------------------------------------------------------------------------
+
+
+def to_device_i64(a, device):
+    torch = _torch()
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device, dtype=torch.int64)
+    return torch.as_tensor(np.asarray(a, dtype=np.int64), device=device)
+
+
+def rope_table(positions, d_head: int, base: float, device) -> "object":
+    """fp32 (cos, sin) table [n, d_head/2, 2], angles in fp64 on device."""
+    torch = _torch()
+    pos = to_device_i64(positions, device).contiguous()
+    cs = torch.empty((pos.numel(), d_head // 2, 2), dtype=torch.float32, device=device)
+    N.call("ifkv_rope_table", N.ptr(pos), pos.numel(), d_head, float(base), N.ptr(cs), _s())
+    return cs
+
+
+def rotate_rows(src, dst, row_table, cs):
+    """Kernel 1 over [L, T, Hkv, Dh] slabs (dst may be src: in place)."""
+    L, T, Hkv, Dh = src.shape
+    if T == 0:
+        return dst
+    N.call("ifkv_rotate_rows", dt_code(src), N.ptr(src), N.ptr(dst), src.stride(0), L, T, Hkv, Dh,
+           N.ptr(row_table), N.ptr(cs), _s())
+    return dst
+
+
+def assemble_gather(src_keys: Sequence, src_values: Sequence, dst_k, dst_v, row0: Sequence[int]):
+    import ctypes as C
+
+    n = len(src_keys)
+    if n == 0:
+        return
+    L, _, Hkv, Dh = dst_k.shape
+    pk = (C.c_void_p * n)(*[t.data_ptr() for t in src_keys])
+    pv = (C.c_void_p * n)(*[t.data_ptr() for t in src_values])
+    strides = (C.c_int64 * n)(*[t.stride(0) for t in src_keys])
+    lens = (C.c_int32 * n)(*[t.shape[1] for t in src_keys])
+    r0 = (C.c_int32 * n)(*[int(r) for r in row0])
+    for tk, tv in zip(src_keys, src_values):
+        for t in (tk, tv):
+            if (t.stride(3), t.stride(2), t.stride(1)) != (1, Dh, Hkv * Dh) or t.dtype != dst_k.dtype:
+                raise ConfigurationError("chunk KV rows must be contiguous [L, len, Hkv, Dh] of the slab dtype")
+        if tk.stride(0) != tv.stride(0):
+            raise ConfigurationError("chunk keys and values must share a layer stride")
+    N.call("ifkv_assemble_gather", dt_code(dst_k), n, C.cast(pk, C.c_void_p), C.cast(pv, C.c_void_p),
+           C.cast(strides, C.c_void_p), C.cast(lens, C.c_void_p), C.cast(r0, C.c_void_p), N.ptr(dst_k),
+           N.ptr(dst_v), dst_k.stride(0), L, Hkv * Dh, _s())
+
+
+def add_rmsnorm(h, delta, n_parts: int, gain, out_mode: int):
+    torch = _torch()
+    rows, d = h.shape
+    out = None
+    if out_mode == N.OUT_F32:
+        out = torch.empty((rows, d), dtype=torch.float32, device=h.device)
+    elif out_mode == N.OUT_BF16:
+        out = torch.empty((rows, d), dtype=torch.bfloat16, device=h.device)
+    elif out_mode == N.OUT_SPLIT3:
+        out = torch.empty((3, rows, d), dtype=torch.bfloat16, device=h.device)
+    ddt = dt_code(delta) if delta is not None else N.IFKV_F32
+    N.call("ifkv_add_rmsnorm", N.ptr(h), N.ptr(delta), ddt, n_parts if delta is not None else 0, N.ptr(gain),
+           rows, d, out_mode, N.ptr(out), _s())
+    return out
+
+
+def residual_add(h, delta, n_parts: int):
+    N.call("ifkv_add_rmsnorm", N.ptr(h), N.ptr(delta), dt_code(delta), n_parts, None, h.shape[0], h.shape[1],
+           N.OUT_F32, None, _s())
+
+
+def silu_mul(gu, n_parts: int, d_ff: int, out_mode: int):
+    torch = _torch()
+    rows = gu.shape[-2]
+    shape = (3, rows, d_ff) if out_mode == N.OUT_SPLIT3 else (rows, d_ff)
+    dt = torch.float32 if out_mode == N.OUT_F32 else torch.bfloat16
+    out = torch.empty(shape, dtype=dt, device=gu.device)
+    N.call("ifkv_silu_mul", N.ptr(gu), dt_code(gu), n_parts, rows, d_ff, out_mode, N.ptr(out), _s())
+    return out
+
+
+def embed_rows(table, ids):
+    torch = _torch()
+    ids = ids.contiguous()
+    h = torch.empty((ids.numel(), table.shape[1]), dtype=torch.float32, device=table.device)
+    N.call("ifkv_embed_rows", N.ptr(table), dt_code(table), N.ptr(ids), ids.numel(), table.shape[1], N.ptr(h), _s())
+    return h
+
+
+def split3(x):
+    torch = _torch()
+    out = torch.empty((3,) + tuple(x.shape), dtype=torch.bfloat16, device=x.device)
+    N.call("ifkv_split3", N.ptr(x), x.numel(), N.ptr(out), _s())
+    return out
+
+
+def qkv_rope_scatter(qkv, n_parts, H, Hkv, Dh, cs, q_out, k_dst, v_dst, dst_rows):
+    rows = qkv.shape[-2]
+    out_dt = dt_code(k_dst)
+    N.call("ifkv_qkv_rope_scatter", N.ptr(qkv), dt_code(qkv), n_parts, rows, H, Hkv, Dh, N.ptr(cs), out_dt,
+           N.ptr(q_out), N.ptr(k_dst), N.ptr(v_dst), N.ptr(dst_rows), _s())
+
+
+def topk_segments(scores, seg_begin, seg_k, agg_mode: int = N.AGG_NONE):
+    """Segmented exact top-k; seg_begin/seg_k are host int sequences."""
+    torch = _torch()
+    dev = scores.device
+    seg_begin = np.asarray(seg_begin, dtype=np.int32)
+    seg_k = np.asarray(seg_k, dtype=np.int32)
+    out_begin = np.concatenate([[0], np.cumsum(seg_k)]).astype(np.int32)
+    meta = torch.as_tensor(np.concatenate([seg_begin, seg_k, out_begin]), device=dev)
+    nseg = seg_k.size
+    out = torch.empty(int(out_begin[-1]), dtype=torch.int64, device=dev)
+    agg = torch.empty(nseg, dtype=torch.float64, device=dev) if agg_mode != N.AGG_NONE else None
+    base = meta.data_ptr()
+    N.call("ifkv_topk_segments", N.ptr(scores), base, base + 4 * (nseg + 1), base + 4 * (2 * nseg + 1), nseg,
+           N.ptr(out), agg_mode, N.ptr(agg), _s())
+    return out, agg, out_begin
+
+
+def recompute_attn(q, k_layer, v_layer, horizon, H, Hkv, Dh, out=None):
+    torch = _torch()
+    S = q.shape[0]
+    if out is None:
+        out = torch.empty_like(q)
+    N.call("ifkv_recompute_attn", dt_code(q), N.ptr(q), N.ptr(k_layer), N.ptr(v_layer), N.ptr(horizon), S, H, Hkv,
+           Dh, 1.0 / math.sqrt(Dh), N.ptr(out), _s())
+    return out
+
+
+# ---------------------------------------------------------------------------
+# GEMMs (cuBLAS via torch.mm): fp32-accurate variant for the scoring path
+# ---------------------------------------------------------------------------
+
+
+def mm_parts(x, w):
+    """x: [P, rows, K] (bf16 split terms) or [rows, K] fp32; returns fp32
+    [P, rows, N] (sum the P blocks downstream) -- exact products, fp32 sums."""
+    torch = _torch()
+    if x.dim() == 3:
+        p, rows, k = x.shape
+        y = torch.mm(x.reshape(p * rows, k), w, out_dtype=torch.float32)
+        return y.view(p, rows, w.shape[1])
+    return torch.mm(x, w).unsqueeze(0)
+
+
+# ---------------------------------------------------------------------------
+# Prompt forward over an injected prefix
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class PromptGroup:
+    """One independent prompt run: its tokens/positions and the slab rows it
+    attends, as runs (row0, n_rows, delta) where keys are read as
+    R(delta) k_stored."""
+
+    token_ids: np.ndarray
+    positions: np.ndarray
+    segments: List[Tuple[int, int, int]]
+
+
+@dataclass
+class PromptOut:
+    scores: Optional["object"] = None  # fp32 [T] indexed by slab row (capture layer)
+    logits: Optional["object"] = None  # fp32 [G, vocab] (last prompt row of each group)
+    ml: Optional["object"] = None
+
+
+def segments_from_deltas(deltas: np.ndarray, row_offset: int = 0) -> List[Tuple[int, int, int]]:
+    """Runs of constant rotation delta over rows row_offset + [0, len)."""
+    deltas = np.asarray(deltas, dtype=np.int64)
+    if deltas.size == 0:
+        return []
+    cut = np.flatnonzero(np.diff(deltas)) + 1
+    starts = np.concatenate([[0], cut])
+    ends = np.concatenate([cut, [deltas.size]])
+    return [(row_offset + int(a), int(b - a), int(deltas[a])) for a, b in zip(starts, ends)]
+
+
+def _plan_items(groups: Sequence[PromptGroup], M: int):
+    """Work items (24-byte ifkv_attn_item rows), query sets and deltas."""
+    deltas = sorted({d for g in groups for (_, _, d) in g.segments if d != 0})
+    delta_id = {d: i for i, d in enumerate(deltas)}
+    qset_group, qset_cs, qset_of = [], [], {}
+
+    def qset(gi, d):
+        key = (gi, d)
+        if key not in qset_of:
+            qset_of[key] = len(qset_group)
+            qset_group.append(gi)
+            qset_cs.append(delta_id[d] if d != 0 else -1)
+        return qset_of[key]
+
+    items, item_begin = [], [0]
+    for gi, g in enumerate(groups):
+        for row0, n, d in g.segments:
+            qs = qset(gi, d)
+            for off in range(0, n, ITEM_KEYS):
+                items.append((gi, qs, row0 + off, min(ITEM_KEYS, n - off), 0, 1))
+        items.append((gi, qset(gi, 0), 0, M, 1, 0))
+        item_begin.append(len(items))
+    return (np.asarray(items, dtype=np.int32).reshape(-1, 6), np.asarray(item_begin, np.int32),
+            np.asarray(qset_group, np.int32), np.asarray(qset_cs, np.int32), deltas)
+
+
+def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], capture_layer: Optional[int] = None,
+                   want_logits: bool = False) -> PromptOut:
+    """Run every group's prompt forward; capture column scores at
+    ``capture_layer`` (then stop) or return last-row logits."""
+    torch = _torch()
+    cfg = weights.config
+    dev = weights.device
+    H, Hkv, Dh, d = cfg.n_heads, cfg.kv_heads, cfg.d_head, cfg.d_model
+    G = len(groups)
+    M = int(np.asarray(groups[0].token_ids).size)
+    if any(int(np.asarray(g.token_ids).size) != M for g in groups):
+        raise ConfigurationError("all prompt groups must have the same length")
+    bf16 = weights.precision == "bf16"
+    mode = N.OUT_SPLIT3 if bf16 else N.OUT_F32
+    items_np, item_begin_np, qg_np, qc_np, deltas = _plan_items(groups, M)
+    n_items, n_qsets = items_np.shape[0], qg_np.size
+    meta = torch.as_tensor(np.concatenate([items_np.ravel(), item_begin_np, qg_np, qc_np]), device=dev)
+    items_p = meta.data_ptr()
+    ib_p = items_p + 4 * items_np.size
+    qg_p = ib_p + 4 * item_begin_np.size
+    qc_p = qg_p + 4 * qg_np.size
+    cs_delta = rope_table(np.asarray(deltas, np.int64) if deltas else np.zeros(1, np.int64), Dh, cfg.rope_base, dev)
+    ids = torch.as_tensor(np.concatenate([np.asarray(g.token_ids, np.int64) for g in groups]), device=dev)
+    cs_prompt = rope_table(np.concatenate([np.asarray(g.positions, np.int64) for g in groups]), Dh, cfg.rope_base, dev)
+    pos_all = np.concatenate([np.asarray(g.positions, np.int64) for g in groups])
+    if pos_all.min() < 0 or pos_all.max() >= cfg.max_position:
+        raise ConfigurationError(f"position outside [0, {cfg.max_position}): {int(pos_all.max())}")
+    if capture_layer is not None and not 0 <= capture_layer < cfg.n_layers:
+        raise ConfigurationError(f"capture layer {capture_layer} outside [0, {cfg.n_layers})")
+    rows = G * M
+    h = embed_rows(weights.embedding, ids)
+    q = torch.empty((rows, H, Dh), dtype=torch.float32, device=dev)
+    kp = torch.empty((rows, Hkv, Dh), dtype=torch.float32, device=dev)
+    vp = torch.empty_like(kp)
+    qd = torch.empty((n_qsets, H, M, Dh), dtype=torch.float32, device=dev)
+    part_ml = torch.empty((n_items, H, M, 2), dtype=torch.float32, device=dev)
+    part_o = torch.empty((n_items, H, M, Dh), dtype=torch.float32, device=dev)
+    ctx = torch.empty((G, M, H, Dh), dtype=torch.float32, device=dev)
+    ml = torch.empty((G, H, M, 2), dtype=torch.float32, device=dev)
+    scale = 1.0 / math.sqrt(Dh)
+    kv_dt = dt_code(slab_k)
+    pending, pending_parts = None, 0
+    last = cfg.n_layers - 1 if capture_layer is None else capture_layer
+    out = PromptOut()
+    for li in range(last + 1):
+        lw = weights.layers[li]
+        x = add_rmsnorm(h, pending, pending_parts, lw.attn_norm, mode)
+        qkv = mm_parts(x, lw.wqkv)
+        qkv_rope_scatter(qkv, qkv.shape[0], H, Hkv, Dh, cs_prompt, q, kp, vp, None)
+        N.call("ifkv_rotate_queries", N.ptr(q), G, M, H, Dh, qg_p, qc_p, n_qsets, N.ptr(cs_delta), N.ptr(qd), _s())
+        N.call("ifkv_prompt_attn_partial", kv_dt, N.ptr(qd), N.ptr(slab_k[li]), N.ptr(slab_v[li]), N.ptr(kp),
+               N.ptr(vp), items_p, n_items, H, Hkv, M, Dh, scale, N.ptr(part_ml), N.ptr(part_o), _s())
+        N.call("ifkv_prompt_attn_merge", N.ptr(part_ml), N.ptr(part_o), ib_p, G, H, M, Dh, N.ptr(ctx), N.ptr(ml),
+               _s())
+        if capture_layer is not None and li == capture_layer:
+            scores = torch.zeros(slab_k.shape[1], dtype=torch.float32, device=dev)
+            N.call("ifkv_score_columns", kv_dt, N.ptr(qd), N.ptr(slab_k[li]), items_p, n_items, N.ptr(ml), H, Hkv,
+                   M, Dh, scale, N.ptr(scores), _s())
+            out.scores, out.ml = scores, ml
+            return out
+        cx = split3(ctx.view(rows, d)) if bf16 else ctx.view(rows, d)
+        o = mm_parts(cx, lw.wo)
+        x2 = add_rmsnorm(h, o, o.shape[0], lw.mlp_norm, mode)
+        gu = mm_parts(x2, lw.wgu)
+        a = silu_mul(gu, gu.shape[0], cfg.d_ff, mode)
+        pending = mm_parts(a, lw.wdown)
+        pending_parts = pending.shape[0]
+    if want_logits:
+        fin = add_rmsnorm(h, pending, pending_parts, weights.final_norm, mode)
+        last_rows = fin[..., M - 1::M, :] if bf16 else fin[M - 1::M]
+        out.logits = mm_parts(last_rows.contiguous(), weights.out_head).sum(0)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Layer stack for S tokens with in-place K/V scatter (recompute / prefill)
+# ---------------------------------------------------------------------------
+
+
+def layer_stack(weights, token_ids, positions, k_slab, v_slab, dst_rows, horizon, want_hidden: bool = False):
+    """Advance S tokens (device int64 ids/positions) through every layer.
+
+    Layer l: x = rms_norm(h); q,k,v = x W; rope at ``positions``; k,v written
+    to slab rows ``dst_rows`` (so later tokens see them); attention of q over
+    slab keys 0..horizon[i]; residual O-proj and MLP.  The last layer stops
+    after its K/V (nothing else can change a K/V row).
+    """
+    torch = _torch()
+    cfg = weights.config
+    dev = weights.device
+    H, Hkv, Dh, d = cfg.n_heads, cfg.kv_heads, cfg.d_head, cfg.d_model
+    S = int(token_ids.numel())
+    if S == 0:
+        return None
+    bf16 = weights.precision == "bf16"
+    act_mode = N.OUT_BF16 if bf16 else N.OUT_F32
+    cs = rope_table(positions, Dh, cfg.rope_base, dev)
+    h = embed_rows(weights.embedding, token_ids)
+    qbuf = torch.empty((S, H, Dh), dtype=weights.torch_dtype, device=dev)
+    attn_out = torch.empty_like(qbuf)
+    pending = None
+    for li, lw in enumerate(weights.layers):
+        final = li == cfg.n_layers - 1 and not want_hidden
+        x = add_rmsnorm(h, pending, 1, lw.attn_norm, act_mode)
+        qkv = torch.mm(x, lw.wqkv)
+        qkv_rope_scatter(qkv, 1, H, Hkv, Dh, cs, None if final else qbuf, k_slab[li], v_slab[li], dst_rows)
+        if final:
+            return None
+        recompute_attn(qbuf, k_slab[li], v_slab[li], horizon, H, Hkv, Dh, out=attn_out)
+        o = torch.mm(attn_out.view(S, d), lw.wo, out_dtype=torch.float32) if bf16 else torch.mm(attn_out.view(S, d),
+                                                                                                 lw.wo)
+        x2 = add_rmsnorm(h, o, 1, lw.mlp_norm, act_mode)
+        gu = torch.mm(x2, lw.wgu)
+        a = silu_mul(gu, 1, cfg.d_ff, act_mode)
+        pending = torch.mm(a, lw.wdown, out_dtype=torch.float32) if bf16 else torch.mm(a, lw.wdown)
+    residual_add(h, pending, 1)
+    return h
