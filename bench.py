@@ -1,0 +1,414 @@
+"""Benchmark: InfoFlow-KV query-time context assembly on B200.
+
+Metric (BASELINE.json): assemble + select + recompute time and ctx tok/s for
+a Llama-3-8B-shaped model (random-init bf16 weights), a 32K-token context of
+16 x 2048 chunks (synthetic uniform-noise tokens from the reference's task
+generator) and a 15% recompute ratio, on one B200.  A step = one pass of the
+path over the prepared (HBM-resident) chunk KVs: assemble -> attention-norm
+selection (fp32-accurate prompt forward to layer 19 + exact top-k) ->
+selective recompute of 4916 tokens through 32 layers with in-place K/V
+scatter.  value = context tokens / step time, summed over ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Under torchrun each rank runs an independent replica (chunk sharding of one
+context is a later milestone).  Rank 0 prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS = {"hbm_gbs": 6534.1, "bf16_tflops": 1659.4, "bf16_tflops_sustained": 1395.0, "source": "fallback"}
+try:
+    _p = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    PEAKS.update({k: _p[k] for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained") if k in _p})
+    PEAKS["source"] = "measured (MEASURED_PEAKS.json)"
+except Exception:
+    pass
+
+METRIC = "assemble+select+recompute ms & ctx tok/s, Llama-3-8B shape, 32K ctx, 15% recompute"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--ctx", type=int, default=32768)
+    ap.add_argument("--chunk", type=int, default=2048)
+    ap.add_argument("--ratio", type=float, default=0.15)
+    ap.add_argument("--layers", type=int, default=32, help="override model depth (debug only)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:]) if v.lower() == "active"})
+        mx = next((float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()), None)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_setup():
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+
+def run_ours(args, world, rank, local):
+    import torch
+
+    import paper_2603_05353_b200 as P
+    from paper_2603_05353_b200 import _native as N
+    from paper_2603_05353_b200 import engine as E
+
+    cfg = P.llama3_8b_config()
+    if args.layers != 32:
+        import dataclasses
+
+        cfg = dataclasses.replace(cfg, n_layers=args.layers)
+    weights = P.DeviceWeights.random(cfg, seed=7, precision="bf16")
+    task = P.SyntheticTask(kind="uniform_noise", total_length=args.ctx, fixed_size=args.chunk, prompt_length=32,
+                           vocab_size=cfg.vocab_size)
+    gen = P.generate_task(task, seed=rank)
+    chunks, prompt = gen.chunks, gen.prompt_token_ids
+    chunk_kvs = [P.prefill_chunk(weights, c) for c in chunks]  # prepared context (not timed)
+    sel_cfg = P.SelectionConfig(ratio=args.ratio)
+    n_ctx = sum(c.local_length for c in chunks)
+    torch.cuda.synchronize()
+
+    def step(timer=None):
+        return P.assemble_select_recompute(weights, chunk_kvs, chunks, prompt, sel_cfg, timer=timer)
+
+    for _ in range(args.warmup):
+        res = step()
+    del res
+    torch.cuda.synchronize()
+
+    # stage breakdown + kernel brackets (separate, untimed pass)
+    timer = P.StageTimer()
+    E.PROFILE = {}
+    res = step(timer)
+    torch.cuda.synchronize()
+    stages = timer.durations_ms()
+    sel_h = res.selection.selected_numpy()
+    prof = E.PROFILE
+    E.PROFILE = None
+    attn = prof.get("recompute_attn", [])
+    attn_ms = [a.elapsed_time(b) for a, b, _ in attn]
+    rot = prof.get("rotate_rows", [])
+    rot_ms = [a.elapsed_time(b) for a, b, _ in rot]
+    del res
+
+    # timed region
+    barrier(world)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    launches0 = N.LAUNCH_COUNT[0]
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        res = step()
+        del res
+    ev1.record()
+    torch.cuda.synchronize()
+    launches = N.LAUNCH_COUNT[0] - launches0
+    clk = clocks.stop()
+    barrier(world)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    ms = max_over_ranks(ms, world)
+    value = n_ctx * world / (ms / 1e3)
+
+    # e2e through the public API with host buffers in and out
+    e2e = None
+    if not args.no_e2e:
+        times = []
+        h2d = d2h = 0
+        for _ in range(max(2, min(args.steps, 5))):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = P.assemble_select_recompute(weights, chunk_kvs, chunks, np.array(prompt), sel_cfg)
+            sel_host = res.selection.selected_numpy()
+            sc_host = res.selection.scores_numpy()
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+            h2d = prompt.nbytes + res.cache.token_ids.nbytes
+            d2h = sel_host.size * 8 + sc_host.size * 4
+            del res
+        e2e_ms = max_over_ranks(statistics.median(times) * 1e3, world)
+        e2e = {"value": n_ctx * world / (e2e_ms / 1e3), "unit": "ctx tok/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    # roofline of the dominant kernel of ours: recompute attention (tensor-bound)
+    H, Dh, L = cfg.n_heads, cfg.d_head, cfg.n_layers
+    flops_per_launch = 4.0 * H * Dh * float(np.sum(sel_h + 1))
+    attn_avg_ms = float(np.mean(attn_ms)) if attn_ms else None
+    achieved = flops_per_launch / (attn_avg_ms / 1e3) / 1e12 if attn_avg_ms else None
+    peak = PEAKS["bf16_tflops_sustained"]
+    roof = {"kernel": "ifkv recompute_attn (tcgen05)", "bound": "tensor", "achieved": achieved, "peak": peak,
+            "unit": "TFLOP/s", "frac": achieved / peak if achieved else None, "traffic": None,
+            "peak_source": PEAKS["source"] + " sustained bf16",
+            "algorithmic_flops_per_launch": flops_per_launch, "avg_launch_ms": attn_avg_ms,
+            "launches_per_step": len(attn_ms), "share_of_step": float(np.sum(attn_ms)) / ms if attn_ms else None}
+    rot_bytes = 2.0 * n_ctx * L * cfg.kv_heads * Dh * 2 * (1 - args.chunk / n_ctx)  # first chunk has delta 0
+    rot_roof = None
+    if rot_ms:
+        ach = rot_bytes / (float(np.mean(rot_ms)) / 1e3) / 1e9
+        rot_roof = {"kernel": "ifkv rotate_rows (Kernel 1)", "bound": "hbm", "achieved": ach, "peak": PEAKS["hbm_gbs"],
+                    "unit": "GB/s", "frac": ach / PEAKS["hbm_gbs"], "avg_launch_ms": float(np.mean(rot_ms)),
+                    "algorithmic_bytes_per_launch": rot_bytes}
+
+    # comparator: full bf16 prefill of the same context through the same kernels
+    torch.cuda.synchronize()
+    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    toks = np.concatenate([c.token_ids for c in chunks])
+    ea.record()
+    full = P.full_prefill(weights, toks)
+    eb.record()
+    torch.cuda.synchronize()
+    full_ms = ea.elapsed_time(eb)
+    del full
+
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "ctx tok/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (reference generate_task uniform_noise tokens; random-init weights, GPU-drawn N(0,1)/sqrt(fan_in))",
+        "config": {"workload": "C2: Llama-3-8B shape (32L, 32q/8kv heads, d_ff 14336), 32K ctx = 16 x 2048 chunks, "
+                               "32-token prompt, 15% recompute (k=%d), norm layer 19" % sel_h.size,
+                   "ctx_tokens": n_ctx, "chunks": len(chunks), "recompute_ratio": args.ratio,
+                   "selected": int(sel_h.size), "parallelism": f"replicas x{world}",
+                   "l2": "inputs larger than L2 (4.3 GB KV slab + 16 GB weights per step)"},
+        "stages_ms": stages,
+        "full_prefill_ms": full_ms,
+        "ratio_vs_full_prefill": ms / full_ms,
+        "roofline": roof,
+        "roofline_kernel1": rot_roof,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    return line
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle (NumPy port of the reference) on a bounded sample
+# ---------------------------------------------------------------------------
+
+
+def cpu_sample_setup(args, seed=0):
+    """Inputs of the CPU sample: a 2-layer model at Llama-3-8B width (f32),
+    the full context's chunk KVs for those 2 layers, a prompt."""
+    import oracle as O
+
+    try:
+        from threadpoolctl import threadpool_info
+
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        threads = os.cpu_count() or 1
+    rng = np.random.default_rng(seed)
+    d, h, hkv, dh, dff, vocab = 4096, 32, 8, 128, 14336, 4096
+    n, m, chunk = args.ctx, 32, args.chunk
+    k = int(np.ceil(args.ratio * n))
+
+    class Cfg:
+        n_layers, n_heads, n_kv_heads, d_head, d_model, d_ff, vocab_size = 2, h, hkv, dh, d, dff, vocab
+        rope_base, max_position = 500000.0, 1 << 20
+
+    class Layer:
+        pass
+
+    def mat(r, c, s):
+        return (rng.standard_normal((r, c), dtype=np.float32) * np.float32(s))
+
+    layers = []
+    for _ in range(2):
+        lw = Layer()
+        lw.attn_norm = np.ones(d, np.float32)
+        lw.mlp_norm = np.ones(d, np.float32)
+        lw.wq, lw.wk, lw.wv, lw.wo = mat(d, d, d ** -0.5), mat(d, hkv * dh, d ** -0.5), mat(d, hkv * dh, d ** -0.5), \
+            mat(d, d, d ** -0.5)
+        lw.w_gate, lw.w_up, lw.w_down = mat(d, dff, d ** -0.5), mat(d, dff, d ** -0.5), mat(dff, d, dff ** -0.5)
+        layers.append(lw)
+
+    class W:
+        pass
+
+    w = W()
+    w.config, w.layers = Cfg, layers
+    w.embedding = mat(vocab, d, 1.0)
+    w.final_norm, w.out_head = np.ones(d, np.float32), mat(d, 8, 1.0)
+    chunks = []
+    for c in range(n // chunk):
+        kk = rng.standard_normal((2, chunk, hkv, dh), dtype=np.float32)
+        vv = rng.standard_normal((2, chunk, hkv, dh), dtype=np.float32)
+        chunks.append(O.Chunk(f"c{c}", rng.integers(0, vocab, chunk), kk, vv, np.arange(chunk), 0))
+    prompt = rng.integers(0, vocab, m)
+    sel = np.sort(rng.choice(n, k, replace=False))[::8]  # 1/8 of the selected rows (cost is linear in rows)
+    return dict(w=w, chunks=chunks, prompt=prompt, sel=sel, threads=threads, n=n, m=m, chunk=chunk, k=k)
+
+
+def cpu_sample(args, inp):
+    """One scoring pass (layer 0 full + layer 1 captured) and one recompute
+    pass (layer 0 full + layer 1 K/V) at Llama-3-8B width on the full context
+    (oracle, f32, all host threads), extrapolated to the 32-layer path with
+    norm layer 19: t = asm + (19 + 0.3)/1.3 x score2 + (31 + 0.1)/1.1 x rec2.
+    Returns (extrapolated seconds, sample description, threads)."""
+    import oracle as O
+
+    w, chunks, prompt, sel = inp["w"], inp["chunks"], inp["prompt"], inp["sel"]
+    threads, n, m, chunk, k = inp["threads"], inp["n"], inp["m"], inp["chunk"], inp["k"]
+    t0 = time.perf_counter()
+    cache = O.assemble(chunks)
+    t_asm = time.perf_counter() - t0
+    ctx, prm = O.assign_positions("GLOBAL", [chunk] * (n // chunk), m)
+    t0 = time.perf_counter()
+    O.score_attention_norm(w, cache, prompt, np.concatenate(ctx), prm, norm_layer=1)
+    t_score2 = time.perf_counter() - t0  # layer 0 full + layer 1 capture ~ 1.3 layers
+    t0 = time.perf_counter()
+    O.recompute_selected(w, cache, sel)
+    t_rec2 = 8.0 * (time.perf_counter() - t0)  # 1/8 of the rows; layer 0 full + layer 1 K/V only
+    t_total = t_asm + (19 + 0.3) / 1.3 * t_score2 + (31 + 0.1) / 1.1 * t_rec2
+    desc = (f"oracle f32 on {threads} threads: Llama-3-8B width, 2 layers, {n} ctx, k={k}; measured assemble "
+            f"{t_asm:.2f}s, 2-layer scoring {t_score2:.2f}s, 2-layer recompute of k/8 rows x 8 = {t_rec2:.2f}s; "
+            f"extrapolated to "
+            f"32 layers / norm layer 19 as asm + 14.8 x score2 + 28.3 x rec2")
+    return t_total, desc, threads
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return None
+    times = []
+    desc, threads = "", 1
+    inp = cpu_sample_setup(args)
+    for i in range(args.warmup + args.steps):
+        t, desc, threads = cpu_sample(args, inp)
+        if i >= args.warmup:
+            times.append(t)
+    t = statistics.median(times)
+    value = args.ctx / t
+    return {"metric": METRIC, "value": value, "unit": "ctx tok/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+            "config": {"workload": "C2 sample (see cpu_baseline.sample)", "ctx_tokens": args.ctx},
+            "cpu_baseline": {"value": value, "unit": "ctx tok/s", "cores": threads, "kind": "port", "sample": desc},
+            "e2e": {"value": value, "unit": "ctx tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        line = run_reference(args, world, rank)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    world, rank, local = dist_setup()
+    line = run_ours(args, world, rank, local)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        t, desc, threads = cpu_sample(args, cpu_sample_setup(args))
+        line["cpu_baseline"] = {"value": args.ctx / t, "unit": "ctx tok/s", "cores": threads, "kind": "port",
+                                "sample": desc}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -152,11 +152,18 @@ int ifkv_topk_segments(const float* scores, const int32_t* seg_begin, const int3
 
 /* ---- selective recompute attention (recompute.py:92-114) ----------------
  * Query row i (head h) attends keys 0..horizon[i] of the layer's K/V view
- * [N][Hkv][Dh] (kv head h / (H/Hkv)); horizons ascending.
+ * [n_rows][Hkv][Dh] (kv head h / (H/Hkv)); horizons ascending, < n_rows.
  * q [S][H][Dh], out [S][H][Dh], element type dtype, fp32 softmax. */
 int ifkv_recompute_attn(int dtype, const void* q, const void* k_layer, const void* v_layer,
-                        const int64_t* horizon, int S, int H, int Hkv, int Dh, float scale, void* out,
+                        const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows, float scale, void* out,
                         void* stream);
+/* The two implementations behind it (selected automatically): the tcgen05 /
+ * TMEM / TMA kernel for bf16, Dh = 128, H/Hkv in {1,2,4,8}; and the generic
+ * SIMT fp32-softmax kernel (fp32 mode, other head sizes). */
+int ifkv_recompute_attn_tc_supported(int dtype, int H, int Hkv, int Dh);
+int ifkv_recompute_attn_simt(int dtype, const void* q, const void* k_layer, const void* v_layer,
+                             const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows, float scale,
+                             void* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -38,8 +38,8 @@ SIGNATURES = {
     "ifkv_score_columns": [I32, P, P, P, I32, P, I32, I32, I32, I32, F32, P, P],
     "ifkv_rotate_queries": [P, I32, I32, I32, I32, P, P, I32, P, P, P],
     "ifkv_topk_segments": [P, P, P, P, I32, P, I32, P, P],
-    "ifkv_recompute_attn": [I32, P, P, P, P, I32, I32, I32, I32, F32, P, P],
-    "ifkv_recompute_attn_simt": [I32, P, P, P, P, I32, I32, I32, I32, F32, P, P],
+    "ifkv_recompute_attn": [I32, P, P, P, P, I32, I32, I32, I32, I32, F32, P, P],
+    "ifkv_recompute_attn_simt": [I32, P, P, P, P, I32, I32, I32, I32, I32, F32, P, P],
     "ifkv_recompute_attn_tc_supported": [I32, I32, I32, I32],
 }
 EXPORTS = tuple(SIGNATURES) + ("ifkv_last_error", "ifkv_abi_version")
@@ -71,9 +71,14 @@ def load(path: Path = LIB_PATH):
         return lib
 
 
+LAUNCH_COUNT = [0]  # entry-point calls that enqueue kernels (bench gpu_launches)
+
+
 def call(name: str, *args) -> int:
     """Invoke an entry point and translate its status code."""
     lib = load()
+    if not name.endswith("_supported"):
+        LAUNCH_COUNT[0] += 1
     status = getattr(lib, name)(*args)
     if status == 0 or name.endswith("_supported"):
         return status

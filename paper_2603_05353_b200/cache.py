@@ -262,7 +262,8 @@ def to_decode_layout(cache: AssembledCache, rope_base: float) -> AssembledCache:
     delta = decode_targets(cache) - cache.row_positions
     if np.any(delta):
         tab, cs = _delta_table(delta, cache.keys.shape[3], rope_base, cache.keys.device)
-        E.rotate_rows(cache.keys, cache.keys, tab, cs)
+        with E._Bracket("rotate_rows", int(np.count_nonzero(delta))):
+            E.rotate_rows(cache.keys, cache.keys, tab, cs)
         cache.row_positions[:] = decode_targets(cache)
     return cache
 

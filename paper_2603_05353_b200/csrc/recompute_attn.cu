@@ -97,12 +97,11 @@ __global__ void __launch_bounds__(128) recompute_attn_simt_kernel(const T* __res
 using namespace ifkv;
 
 extern "C" int ifkv_recompute_attn_tc(const void* q, const void* k_layer, const void* v_layer, const int64_t* horizon,
-                                      int S, int H, int Hkv, int Dh, float scale, void* out, void* stream);
-extern "C" int ifkv_recompute_attn_tc_supported(int dtype, int H, int Hkv, int Dh);
+                                      int S, int H, int Hkv, int Dh, int n_rows, float scale, void* out, void* stream);
 
 extern "C" int ifkv_recompute_attn_simt(int dtype, const void* q, const void* k_layer, const void* v_layer,
-                                        const int64_t* horizon, int S, int H, int Hkv, int Dh, float scale, void* out,
-                                        void* stream) {
+                                        const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows, float scale,
+                                        void* out, void* stream) {
   IFKV_CHECK_ARG(dtype == IFKV_F32 || dtype == IFKV_BF16, "recompute_attn: bad dtype");
   IFKV_CHECK_ARG(Dh % 2 == 0 && Dh <= 256 && Hkv > 0 && H % Hkv == 0, "recompute_attn: bad shape");
   if (S <= 0) return IFKV_OK;
@@ -125,9 +124,9 @@ extern "C" int ifkv_recompute_attn_simt(int dtype, const void* q, const void* k_
 }
 
 extern "C" int ifkv_recompute_attn(int dtype, const void* q, const void* k_layer, const void* v_layer,
-                                   const int64_t* horizon, int S, int H, int Hkv, int Dh, float scale, void* out,
-                                   void* stream) {
+                                   const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows, float scale,
+                                   void* out, void* stream) {
   if (ifkv_recompute_attn_tc_supported(dtype, H, Hkv, Dh))
-    return ifkv_recompute_attn_tc(q, k_layer, v_layer, horizon, S, H, Hkv, Dh, scale, out, stream);
-  return ifkv_recompute_attn_simt(dtype, q, k_layer, v_layer, horizon, S, H, Hkv, Dh, scale, out, stream);
+    return ifkv_recompute_attn_tc(q, k_layer, v_layer, horizon, S, H, Hkv, Dh, n_rows, scale, out, stream);
+  return ifkv_recompute_attn_simt(dtype, q, k_layer, v_layer, horizon, S, H, Hkv, Dh, n_rows, scale, out, stream);
 }

@@ -29,6 +29,28 @@ from .errors import ConfigurationError
 
 ITEM_KEYS = 128  # keys per prompt-attention work item (<= kItemKeysMax)
 
+# Optional CUDA-event brackets around named kernels: {name: [(start, end, work)]}
+# (the benchmark sets this to measure per-launch durations for the roofline).
+PROFILE = None
+
+
+class _Bracket:
+    def __init__(self, name, work=None):
+        self.name, self.work = name, work
+
+    def __enter__(self):
+        if PROFILE is not None:
+            torch = _torch()
+            self.ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            self.ev[0].record()
+        return self
+
+    def __exit__(self, *exc):
+        if PROFILE is not None:
+            self.ev[1].record()
+            PROFILE.setdefault(self.name, []).append((self.ev[0], self.ev[1], self.work))
+        return False
+
 
 def _torch():
     import torch
@@ -178,13 +200,15 @@ def topk_segments(scores, seg_begin, seg_k, agg_mode: int = N.AGG_NONE):
     return out, agg, out_begin
 
 
-def recompute_attn(q, k_layer, v_layer, horizon, H, Hkv, Dh, out=None):
+def recompute_attn(q, k_layer, v_layer, horizon, H, Hkv, Dh, out=None, impl: str = "auto"):
+    """impl: "auto" (tcgen05 when supported, else SIMT) or "simt"."""
     torch = _torch()
     S = q.shape[0]
     if out is None:
         out = torch.empty_like(q)
-    N.call("ifkv_recompute_attn", dt_code(q), N.ptr(q), N.ptr(k_layer), N.ptr(v_layer), N.ptr(horizon), S, H, Hkv,
-           Dh, 1.0 / math.sqrt(Dh), N.ptr(out), _s())
+    name = "ifkv_recompute_attn" if impl == "auto" else "ifkv_recompute_attn_simt"
+    N.call(name, dt_code(q), N.ptr(q), N.ptr(k_layer), N.ptr(v_layer), N.ptr(horizon), S, H, Hkv, Dh,
+           k_layer.shape[0], 1.0 / math.sqrt(Dh), N.ptr(out), _s())
     return out
 
 
@@ -372,7 +396,8 @@ def layer_stack(weights, token_ids, positions, k_slab, v_slab, dst_rows, horizon
         qkv_rope_scatter(qkv, 1, H, Hkv, Dh, cs, None if final else qbuf, k_slab[li], v_slab[li], dst_rows)
         if final:
             return None
-        recompute_attn(qbuf, k_slab[li], v_slab[li], horizon, H, Hkv, Dh, out=attn_out)
+        with _Bracket("recompute_attn", li):
+            recompute_attn(qbuf, k_slab[li], v_slab[li], horizon, H, Hkv, Dh, out=attn_out)
         o = torch.mm(attn_out.view(S, d), lw.wo, out_dtype=torch.float32) if bf16 else torch.mm(attn_out.view(S, d),
                                                                                                  lw.wo)
         x2 = add_rmsnorm(h, o, 1, lw.mlp_norm, act_mode)

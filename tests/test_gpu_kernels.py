@@ -1,0 +1,160 @@
+"""Kernel-level parity on the GPU: each C-ABI entry point against the oracle
+(or an exact NumPy statement of the same arithmetic) on seeded inputs."""
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def T(cuda):
+    import torch
+
+    return torch
+
+
+def test_rope_table_fp64_angles(T, cuda):
+    from paper_2603_05353_b200 import engine as E
+
+    pos = np.array([0, 1, 7, 4095, 32767, 131071, -5, -2048], dtype=np.int64)
+    for dh, base in ((128, 500000.0), (8, 10000.0), (128, 1e6)):
+        cs = E.rope_table(pos, dh, base, cuda).cpu().numpy()
+        ang = pos[:, None].astype(np.float64) * O.rope_theta(dh, base)[None, :]
+        np.testing.assert_allclose(cs[..., 0], np.cos(ang).astype(np.float32), atol=2e-7)
+        np.testing.assert_allclose(cs[..., 1], np.sin(ang).astype(np.float32), atol=2e-7)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("in_place", [True, False])
+def test_rotate_rows_kernel1(T, cuda, dtype, in_place):
+    from paper_2603_05353_b200 import cache as C
+    from paper_2603_05353_b200 import engine as E
+
+    rng = np.random.default_rng(0)
+    L, n, hkv, dh = 3, 777, 8, 128
+    tdt = T.bfloat16 if dtype == "bf16" else T.float32
+    x = T.as_tensor(rng.standard_normal((L, n, hkv, dh)), dtype=T.float32).to(cuda, tdt)
+    deltas = rng.integers(-3000, 40000, n)
+    deltas[::5] = 0
+    tab, cs = C._delta_table(deltas, dh, 500000.0, cuda)
+    src = x.clone()
+    out = src if in_place else T.empty_like(src)
+    E.rotate_rows(src, out, tab, cs)
+    xs = x.double().cpu().numpy()
+    want = np.stack([O.rope_rotate(xs[l], deltas, 500000.0) for l in range(L)])
+    got = out.double().cpu().numpy()
+    tol = 8e-3 if dtype == "bf16" else 2e-6
+    assert np.max(np.abs(got - want)) <= tol * np.max(np.abs(want))
+    zero = deltas == 0
+    assert np.array_equal(got[:, zero], xs[:, zero])  # delta 0 rows bit-exact
+
+
+def test_assemble_gather_bitwise(T, cuda):
+    from paper_2603_05353_b200 import cache as C
+
+    rng = np.random.default_rng(1)
+    L, hkv, dh = 2, 4, 128
+    lens = [256, 100, 3, 300]
+    chunks = []
+    for i, n in enumerate(lens):
+        k = rng.standard_normal((L, n, hkv, dh))
+        v = rng.standard_normal((L, n, hkv, dh))
+        chunks.append(C.chunk_from_host(f"c{i}", np.arange(n) % 50, k, v, np.arange(n), 0, 123, T.bfloat16))
+    cache = C.assemble(chunks)
+    want_k = T.cat([c.keys for c in chunks], dim=1)
+    want_v = T.cat([c.values for c in chunks], dim=1)
+    assert T.equal(cache.keys, want_k) and T.equal(cache.values, want_v)
+    assert cache.mapping(256) == ("c1", 0) and cache.mapping(358) == ("c2", 2) and cache.mapping(359) == ("c3", 0)
+    perm = C.assemble([chunks[2], chunks[0]])
+    assert T.equal(perm.keys, T.cat([chunks[2].keys, chunks[0].keys], dim=1))
+
+
+def _brute_topk(s, k):
+    return np.sort(np.lexsort((np.arange(s.size), -s))[:k])
+
+
+@pytest.mark.parametrize("n,k", [(1, 0), (1, 1), (10, 3), (2048, 308), (32768, 4916), (131072, 19661),
+                                 (5000, 5000), (4097, 1)])
+def test_topk_exact_with_ties(T, cuda, n, k):
+    from paper_2603_05353_b200.selection import select_topk
+
+    rng = np.random.default_rng(n + k)
+    for trial in range(3):
+        if trial == 0:
+            s = rng.random(n).astype(np.float32)
+        elif trial == 1:
+            s = rng.choice(np.array([0.1, 0.25, 0.5, 0.77], np.float32), size=n)
+        else:
+            s = (rng.random(n) * 1e-3 + 1.0).astype(np.float32)
+            s[rng.integers(0, n, max(1, n // 10))] = 0.0
+        got = select_topk(T.as_tensor(s, device=cuda), k).cpu().numpy()
+        np.testing.assert_array_equal(got, _brute_topk(s.astype(np.float64), k))
+
+
+def test_topk_segments_aggregate(T, cuda):
+    from paper_2603_05353_b200 import _native as N
+    from paper_2603_05353_b200 import engine as E
+
+    rng = np.random.default_rng(5)
+    lens = [256, 2048, 7, 1, 300]
+    s = rng.random(sum(lens)).astype(np.float32)
+    s[260:270] = 0.5
+    begin = np.concatenate([[0], np.cumsum(lens)])
+    ks = [39, 308, 7, 1, 0]
+    for mode in ("sum", "mean", "max"):
+        idx, agg, ob = E.topk_segments(T.as_tensor(s, device=cuda), begin, ks, N.AGG_CODES[mode])
+        idx, agg = idx.cpu().numpy(), agg.cpu().numpy()
+        for i in range(len(lens)):
+            seg = s[begin[i]:begin[i + 1]].astype(np.float64)
+            want = _brute_topk(seg, ks[i])
+            np.testing.assert_array_equal(idx[ob[i]:ob[i + 1]] - begin[i], want)
+            assert agg[i] == pytest.approx(O.aggregate(seg[want], mode), rel=1e-12, abs=0)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("hkv,dh", [(8, 128), (4, 128), (2, 16), (1, 8)])
+def test_recompute_attention_kernel(T, cuda, dtype, hkv, dh):
+    from paper_2603_05353_b200 import engine as E
+
+    rng = np.random.default_rng(hkv * dh)
+    H = 4 * hkv if hkv > 1 else 2
+    n = 1500
+    sel = np.sort(rng.choice(n, 300, replace=False))
+    tdt = T.bfloat16 if dtype == "bf16" else T.float32
+    q = T.as_tensor(rng.standard_normal((sel.size, H, dh)), dtype=T.float32).to(cuda, tdt)
+    k = T.as_tensor(rng.standard_normal((n, hkv, dh)), dtype=T.float32).to(cuda, tdt)
+    v = T.as_tensor(rng.standard_normal((n, hkv, dh)), dtype=T.float32).to(cuda, tdt)
+    out = E.recompute_attn(q, k, v, T.as_tensor(sel, device=cuda), H, hkv, dh)
+    want, _ = O.prefix_attention(q.double().cpu().numpy(), k.double().cpu().numpy(), v.double().cpu().numpy(), sel)
+    got = out.double().cpu().numpy()
+    tol = 1e-2 if dtype == "bf16" else 1e-5
+    assert np.max(np.abs(got - want)) <= tol * np.max(np.abs(want))
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_recompute_attention_tcgen05_vs_simt(T, cuda, G):
+    """The tcgen05 kernel against the SIMT fp32-softmax kernel (and the oracle)
+    on a multi-block causal span: 4096 keys, 700 selected rows."""
+    from paper_2603_05353_b200 import _native as N
+    from paper_2603_05353_b200 import engine as E
+
+    assert N.call("ifkv_recompute_attn_tc_supported", N.IFKV_BF16, 4 * G, 4, 128) == 1
+    rng = np.random.default_rng(G)
+    hkv, dh, n = 4, 128, 4096
+    H = hkv * G
+    sel = np.sort(rng.choice(n, 700, replace=False))
+    q = T.as_tensor(rng.standard_normal((sel.size, H, dh)) * 2, dtype=T.float32).to(cuda, T.bfloat16)
+    k = T.as_tensor(rng.standard_normal((n, hkv, dh)), dtype=T.float32).to(cuda, T.bfloat16)
+    v = T.as_tensor(rng.standard_normal((n, hkv, dh)), dtype=T.float32).to(cuda, T.bfloat16)
+    hz = T.as_tensor(sel, device=cuda)
+    tc = E.recompute_attn(q, k, v, hz, H, hkv, dh).double().cpu().numpy()
+    simt = E.recompute_attn(q, k, v, hz, H, hkv, dh, impl="simt").double().cpu().numpy()
+    want, _ = O.prefix_attention(q.double().cpu().numpy(), k.double().cpu().numpy(), v.double().cpu().numpy(), sel)
+    scale = np.max(np.abs(want))
+    assert np.max(np.abs(simt - want)) <= 1e-2 * scale
+    assert np.max(np.abs(tc - want)) <= 1e-2 * scale

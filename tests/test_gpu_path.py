@@ -1,0 +1,207 @@
+"""End-to-end parity of the GPU path against the oracle on identical inputs.
+
+Inputs: identical weights (device bf16 values, the oracle gets exact float64
+copies) and the GPU's own chunk KVs (the path's input boundary: precomputed
+chunk caches).  Bars (north star): selected index sets and reorder
+permutations bit-exact; scores and recomputed KV within rtol 1e-2 (bf16) /
+1e-4 (fp32 mode), measured as max|a-b| / max|b| per tensor."""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import oracle_cache, oracle_chunk, rel_err, to_np
+
+pytestmark = pytest.mark.gpu
+
+
+def _pkg():
+    import paper_2603_05353_b200 as P
+
+    return P
+
+
+def _setup(cfg, seed_w, precision, task, task_seed, host_weights=None):
+    P = _pkg()
+    hw = host_weights if host_weights is not None else P.init_weights(cfg, seed_w)
+    dw = P.DeviceWeights.from_host(hw, precision)
+    ow = dw.to_host()
+    g = P.generate_task(task, task_seed) if task is not None else None
+    return dw, ow, g
+
+
+C1_TASK = dict(kind="uniform_noise", total_length=2048, fixed_size=256, prompt_length=32, vocab_size=1024)
+
+
+@pytest.fixture(scope="module", params=[0, 1])
+def c1(request, cuda):
+    P = _pkg()
+    dw, ow, g = _setup(P.c1_config(), 7, "bf16", P.SyntheticTask(**C1_TASK), request.param)
+    kvs = [P.prefill_chunk(dw, c) for c in g.chunks]
+    return dw, ow, g, kvs
+
+
+def test_c1_prefill_matches_oracle(c1):
+    dw, ow, g, kvs = c1
+    for ckv, spec in zip(kvs[:2], g.chunks[:2]):
+        want = O.prefill_chunk(ow, spec.chunk_id, spec.token_ids)
+        assert rel_err(to_np(ckv.keys), want.keys) <= 1e-2
+        assert rel_err(to_np(ckv.values), want.values) <= 1e-2
+
+
+def test_c1_selection_bit_exact(c1):
+    P = _pkg()
+    dw, ow, g, kvs = c1
+    cache = P.assemble(kvs)
+    res = P.run_selection(dw, g.chunks, cache, g.prompt_token_ids, P.SelectionConfig(ratio=0.15))
+    oc = O.assemble([oracle_chunk(c) for c in kvs])
+    scores, sel = O.run_selection(ow, oc, g.prompt_token_ids, ratio=0.15)
+    assert rel_err(res.scores_numpy(), scores) <= 1e-4
+    np.testing.assert_array_equal(res.selected_numpy(), sel)
+    assert res.budget == 308
+
+
+def test_c1_recompute_matches_oracle(c1):
+    P = _pkg()
+    dw, ow, g, kvs = c1
+    cache = P.assemble(kvs)
+    res = P.run_selection(dw, g.chunks, cache, g.prompt_token_ids, P.SelectionConfig(ratio=0.15))
+    oc = O.assemble([oracle_chunk(c) for c in kvs])
+    sel = res.selected_numpy()
+    want = O.recompute_selected(ow, oc, *O.make_plan(oc.context_length, sel))
+    wk, wv = O.decode_view(want, dw.config.rope_base)
+    before_k, _ = P.decode_view(cache, dw.config.rope_base)
+    before_k = before_k.clone()
+    out = P.recompute_selected(dw, cache, P.make_plan(cache, res.selected))
+    gk, gv = P.decode_view(out, dw.config.rope_base)
+    assert rel_err(to_np(gk), wk) <= 1e-2
+    assert rel_err(to_np(gv), wv) <= 1e-2
+    keep = np.setdiff1d(np.arange(cache.context_length), sel)
+    assert to_np(gk)[:, keep].tobytes() == to_np(before_k)[:, keep].tobytes()
+    assert (out.provenance[sel] == int(P.Provenance.RECOMPUTED_GLOBAL)).all()
+    assert np.array_equal(out.row_positions[:cache.context_length], np.arange(cache.context_length))
+
+
+def test_c1_reorder_bit_exact(c1):
+    P = _pkg()
+    dw, ow, g, kvs = c1
+    plan, cache, second = P.reorder_and_reselect(dw, g.chunks, g.prompt_token_ids, budget=308, prefilled=kvs)
+    perm, imps, _, scores, sel = O.reorder_and_reselect(ow, [oracle_chunk(c) for c in kvs], g.prompt_token_ids, 308)
+    np.testing.assert_array_equal(plan.permutation, perm)
+    np.testing.assert_allclose(plan.chunk_importance, imps, rtol=1e-4)
+    np.testing.assert_array_equal(second.selected_numpy(), sel)
+    assert rel_err(second.scores_numpy(), scores) <= 1e-4
+
+
+# ---------------------------------------------------------------------------
+# fp32 mode: the reference's tiny configs, 1e-4 bars
+# ---------------------------------------------------------------------------
+
+
+@pytest.fixture(scope="module")
+def tiny(cuda):
+    P = _pkg()
+    cfg = P.ModelConfig(n_layers=2, n_heads=2, d_model=16, d_head=8, d_ff=32, vocab_size=64, max_position=4096)
+    dw, ow, _ = _setup(cfg, 7, "f32", None, None)
+    return P, cfg, dw, ow
+
+
+def test_fp32_golden_direct(tiny, golden_small):
+    """Reference outputs (golden) reproduced from the reference's own chunk KVs."""
+    P, cfg, dw, ow = tiny
+    import torch
+
+    toks, prompt = golden_small["tiny_tokens"], golden_small["tiny_prompt"]
+    chunks = P.make_chunks(toks, [8, 8, 8])
+    kvs = [P.cache.chunk_from_host(f"c{i}", toks[8 * i:8 * i + 8], golden_small["tiny_chunk_keys"][i],
+                                   golden_small["tiny_chunk_values"][i], np.arange(8), 0, dw.fingerprint(),
+                                   torch.float32) for i in range(3)]
+    cache = P.assemble(kvs)
+    for mode, off in (("GLOBAL", None), ("HL-HP", None), ("HL-TP", 200), ("TL-TP", 200)):
+        geo = P.GeometryConfig(mode=mode, prompt_length=4, chunk_lengths=(8, 8, 8), prompt_offset=off)
+        s = P.score_attention_norm(dw, cache, prompt, P.assign_positions(geo, chunks), 1)
+        want = golden_small[f"tiny_scores_{mode}"]
+        assert rel_err(s.double().cpu().numpy(), want) <= 1e-5
+        np.testing.assert_array_equal(P.select_topk(s, 6).cpu().numpy(), golden_small[f"tiny_sel6_{mode}"])
+    out = P.recompute_selected(dw, P.assemble(kvs), P.make_plan(cache, np.array([3, 11, 20])))
+    dk, dv = P.decode_view(out, cfg.rope_base)
+    assert rel_err(to_np(dk), golden_small["tiny_rec_decode_keys"]) <= 1e-4
+    assert rel_err(to_np(dv), golden_small["tiny_rec_values"]) <= 1e-4
+    for budget in (1, 6, 12):
+        plan, _, second = P.reorder_and_reselect(dw, chunks, prompt, budget=budget, prefilled=kvs)
+        np.testing.assert_array_equal(plan.permutation, golden_small[f"tiny_reorder{budget}_perm"])
+        np.testing.assert_array_equal(second.selected_numpy(), golden_small[f"tiny_reorder{budget}_sel"])
+
+
+def test_fp32_full_recompute_equals_full_prefill(tiny):
+    """Criterion 1 (test_acceptance.py:49-63): ratio 1.0 reproduces full prefill."""
+    P, cfg, dw, ow = tiny
+    for seed in range(3):
+        task = P.SyntheticTask(kind="uniform_noise", total_length=256, fixed_size=64, prompt_length=8, vocab_size=64)
+        g = P.generate_task(task, seed)
+        kvs = [P.prefill_chunk(dw, c) for c in g.chunks]
+        cache = P.assemble(kvs)
+        ref = P.full_prefill(dw, cache.token_ids)
+        res = P.run_selection(dw, g.chunks, cache, g.prompt_token_ids, P.SelectionConfig(ratio=1.0))
+        out = P.recompute_selected(dw, cache, P.make_plan(cache, res.selected))
+        assert P.cache_fidelity(out, ref, cfg.rope_base).max_abs <= 1e-4
+
+
+def test_fp32_prefill_and_selection_vs_oracle(tiny):
+    P, cfg, dw, ow = tiny
+    rng = np.random.default_rng(21)
+    toks = rng.integers(0, 64, 32)
+    prompt = rng.integers(0, 64, 4)
+    chunks = P.make_chunks(toks, [8, 8, 8, 8])
+    kvs = [P.prefill_chunk(dw, c) for c in chunks]
+    for ckv, spec in zip(kvs, chunks):
+        want = O.prefill_chunk(ow, spec.chunk_id, spec.token_ids)
+        assert rel_err(to_np(ckv.keys), want.keys) <= 1e-5
+    cache = P.assemble(kvs)
+    res = P.run_selection(dw, chunks, cache, prompt, P.SelectionConfig(topk=10))
+    oc = O.assemble([oracle_chunk(c) for c in kvs])
+    s, sel = O.run_selection(ow, oc, prompt, topk=10)
+    assert rel_err(res.scores_numpy(), s) <= 1e-5
+    np.testing.assert_array_equal(res.selected_numpy(), sel)
+    out = P.recompute_selected(dw, cache, P.make_plan(cache, res.selected))
+    want = O.recompute_selected(ow, oc, *O.make_plan(32, sel))
+    wk, wv = O.decode_view(want, cfg.rope_base)
+    gk, gv = P.decode_view(out, cfg.rope_base)
+    assert rel_err(to_np(gk), wk) <= 1e-4 and rel_err(to_np(gv), wv) <= 1e-4
+
+
+def test_empty_plan_identity_and_validation(tiny):
+    P, cfg, dw, ow = tiny
+    chunks = P.make_chunks(np.arange(16) % 64, [8, 8])
+    cache = P.assemble([P.prefill_chunk(dw, c) for c in chunks])
+    assert P.recompute_selected(dw, cache, P.make_plan(cache, np.array([], np.int64))) is cache
+    with pytest.raises(P.ConfigurationError):
+        P.make_plan(cache, np.array([0, 0]))
+    with pytest.raises(P.ConfigurationError):
+        P.make_plan(cache, np.array([16]))
+    with pytest.raises(P.ConfigurationError):
+        P.select_topk(np.array([1.0]), 2)
+
+
+@pytest.mark.parametrize("precision", ["f32", "bf16"])
+def test_gqa_path_vs_oracle(cuda, precision):
+    P = _pkg()
+    cfg = P.ModelConfig(n_layers=2, n_heads=4, d_model=64, d_head=16, d_ff=96, vocab_size=128, max_position=4096,
+                        n_kv_heads=2)
+    dw, ow, _ = _setup(cfg, 11, precision, None, None)
+    rng = np.random.default_rng(3)
+    toks, prompt = rng.integers(0, 128, 96), rng.integers(0, 128, 8)
+    chunks = P.make_chunks(toks, [32, 32, 32])
+    kvs = [P.prefill_chunk(dw, c) for c in chunks]
+    cache = P.assemble(kvs)
+    res = P.run_selection(dw, chunks, cache, prompt, P.SelectionConfig(ratio=0.2))
+    oc = O.assemble([oracle_chunk(c) for c in kvs])
+    s, sel = O.run_selection(ow, oc, prompt, ratio=0.2)
+    assert rel_err(res.scores_numpy(), s) <= 1e-4
+    np.testing.assert_array_equal(res.selected_numpy(), sel)
+    out = P.recompute_selected(dw, cache, P.make_plan(cache, res.selected))
+    want = O.recompute_selected(ow, oc, *O.make_plan(96, sel))
+    wk, wv = O.decode_view(want, cfg.rope_base)
+    gk, gv = P.decode_view(out, cfg.rope_base)
+    tol = 1e-2 if precision == "bf16" else 1e-4
+    assert rel_err(to_np(gk), wk) <= tol and rel_err(to_np(gv), wv) <= tol
