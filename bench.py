@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--layers", type=int, default=32, help="override model depth (debug only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ncu", action="store_true", help="one warm step inside cudaProfilerStart/Stop, then exit")
     return ap.parse_args()
 
 
@@ -164,6 +165,12 @@ def run_ours(args, world, rank, local):
         res = step()
     del res
     torch.cuda.synchronize()
+    if args.ncu:  # profiler capture range for ncu --profile-from-start off
+        torch.cuda.profiler.start()
+        res = step()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        return None
 
     # stage breakdown + kernel brackets (separate, untimed pass)
     timer = P.StageTimer()
@@ -264,8 +271,9 @@ def run_ours(args, world, rank, local):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (reference generate_task uniform_noise tokens; random-init weights, GPU-drawn N(0,1)/sqrt(fan_in))",
-        "config": {"workload": "C2: Llama-3-8B shape (32L, 32q/8kv heads, d_ff 14336), 32K ctx = 16 x 2048 chunks, "
-                               "32-token prompt, 15% recompute (k=%d), norm layer 19" % sel_h.size,
+        "config": {"workload": f"C2: Llama-3-8B shape ({cfg.n_layers}L, 32q/8kv heads, d_ff 14336), {n_ctx} ctx = "
+                               f"{len(chunks)} x {args.chunk} chunks, 32-token prompt, {args.ratio:.0%} recompute "
+                               f"(k={sel_h.size}), norm layer {P.default_norm_layer(cfg.n_layers)}",
                    "ctx_tokens": n_ctx, "chunks": len(chunks), "recompute_ratio": args.ratio,
                    "selected": int(sel_h.size), "parallelism": f"replicas x{world}",
                    "l2": "inputs larger than L2 (4.3 GB KV slab + 16 GB weights per step)"},
@@ -398,6 +406,8 @@ def main():
         return
     world, rank, local = dist_setup()
     line = run_ours(args, world, rank, local)
+    if line is None:
+        return
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         t, desc, threads = cpu_sample(args, cpu_sample_setup(args))
         line["cpu_baseline"] = {"value": args.ctx / t, "unit": "ctx tok/s", "cores": threads, "kind": "port",

@@ -133,11 +133,13 @@ def test_fp32_golden_direct(tiny, golden_small):
         np.testing.assert_array_equal(second.selected_numpy(), golden_small[f"tiny_reorder{budget}_sel"])
 
 
-def test_fp32_full_recompute_equals_full_prefill(tiny):
+def test_fp32_full_recompute_equals_full_prefill(cuda):
     """Criterion 1 (test_acceptance.py:49-63): ratio 1.0 reproduces full prefill."""
-    P, cfg, dw, ow = tiny
+    P = _pkg()
+    cfg = P.toy_config()
+    dw, ow, _ = _setup(cfg, 7, "f32", None, None)
     for seed in range(3):
-        task = P.SyntheticTask(kind="uniform_noise", total_length=256, fixed_size=64, prompt_length=8, vocab_size=64)
+        task = P.SyntheticTask(kind="uniform_noise", total_length=256, fixed_size=64, prompt_length=8)
         g = P.generate_task(task, seed)
         kvs = [P.prefill_chunk(dw, c) for c in g.chunks]
         cache = P.assemble(kvs)
