@@ -126,19 +126,36 @@ int ifkv_prompt_attn_partial(int kv_dtype, const float* qd, const void* k_slab, 
                              const float* k_prompt, const float* v_prompt, const ifkv_attn_item* items,
                              int n_items, int H, int Hkv, int M, int Dh, float scale, float* part_ml,
                              float* part_o, void* stream);
-/* Merge the partials of each group's items (item_begin [G+1], items sorted by
- * group) in item order: ctx [G][M][H][Dh] fp32 and final ml [G][H][M][2]. */
-int ifkv_prompt_attn_merge(const float* part_ml, const float* part_o, const int32_t* item_begin, int G, int H,
-                           int M, int Dh, float* ctx, float* ml, void* stream);
+/* Merge the partials of each group's items in a fixed order -- its context
+ * items [item_begin[g], item_begin[g+1]) then, if prompt_item0 >= 0, its
+ * prompt item prompt_item0 + g: ctx [G][M][H][Dh] fp32, final ml [G][H][M][2]. */
+int ifkv_prompt_attn_merge(const float* part_ml, const float* part_o, const int32_t* item_begin, int prompt_item0,
+                           int G, int H, int M, int Dh, float* ctx, float* ml, void* stream);
 /* Capture-layer column scores (score_from_attention selection.py:108-124):
  * for each scored item column j, scores[key_row0 + j] =
  * (1/H) sum_h sum_m exp(s_hmj - m_hm) / l_hm, deterministic order. */
 int ifkv_score_columns(int kv_dtype, const float* qd, const void* k_slab, const ifkv_attn_item* items, int n_items,
                        const float* ml, int H, int Hkv, int M, int Dh, float scale, float* scores, void* stream);
 /* Rotated query sets: qd[s] = R(-cs[qset_cs[s]]) q[qset_group[s]], transposed
- * from q [G][M][H][Dh] to [H][M][Dh]; qset_cs[s] < 0 means no rotation. */
+ * from q [G][M][H][Dh] to [H][M][Dh]; qset_cs[s] < 0 means no rotation.
+ * qd3 (optional, bf16 [n_qsets][3][H][M][Dh]) receives the hi/mid/lo split
+ * terms the tensor-core scorer consumes. */
 int ifkv_rotate_queries(const float* q, int G, int M, int H, int Dh, const int32_t* qset_group,
-                        const int32_t* qset_cs, int n_qsets, const float* cs, float* qd, void* stream);
+                        const int32_t* qset_cs, int n_qsets, const float* cs, float* qd, void* qd3, void* stream);
+
+/* Tensor-core (tcgen05/TMEM/TMA) versions for bf16 slabs with Dh = 128:
+ * S = sum_t Q_t K^T and O = sum_t P_t V over hi/mid/lo bf16 terms of the fp32
+ * queries / probabilities (exact products, fp32 sums), one CTA per (context
+ * item, kv head, <=128-row head chunk).  Context items only (prompt items go
+ * to the SIMT kernel).  n_rows = rows of the slab layer view. */
+int ifkv_prompt_attn_tc_supported(int kv_dtype, int H, int Hkv, int M, int Dh);
+int ifkv_prompt_attn_partial_tc(const void* qd3, int n_qsets, const void* k_slab, const void* v_slab, int n_rows,
+                                const ifkv_attn_item* items, int n_items, int H, int Hkv, int M, float scale,
+                                float* part_ml, float* part_o, void* stream);
+/* colsum_ws: fp32 [n_items][Hkv * head_chunks][128] workspace. */
+int ifkv_score_columns_tc(const void* qd3, int n_qsets, const void* k_slab, int n_rows, const ifkv_attn_item* items,
+                          int n_items, const float* ml, int H, int Hkv, int M, float scale, float* colsum_ws,
+                          float* scores, void* stream);
 
 /* ---- top-k (selection.py:172-183) and per-chunk importance
  * (reorder.py:84-112) -----------------------------------------------------

@@ -39,49 +39,101 @@ __device__ __forceinline__ float block_sum_256(float v, float* red) {
   return t;
 }
 
+// Vector helpers: 4 consecutive elements as fp32.
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float4 ld4(const __nv_bfloat16* p) {
+  uint2 u = *reinterpret_cast<const uint2*>(p);
+  __nv_bfloat162 a = *reinterpret_cast<__nv_bfloat162*>(&u.x), b = *reinterpret_cast<__nv_bfloat162*>(&u.y);
+  return make_float4(__low2float(a), __high2float(a), __low2float(b), __high2float(b));
+}
+__device__ __forceinline__ void add4(float4& a, const float4& b) {
+  a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+}
+__device__ __forceinline__ void store4_mode(void* out, int mode, int64_t part_stride, int64_t i, float4 x) {
+  if (mode == IFKV_OUT_F32) {
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + i) = x;
+  } else if (mode == IFKV_OUT_BF16) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(x.x, x.y), b = __floats2bfloat162_rn(x.z, x.w);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(out) + i) = u;
+  } else {
+    __nv_bfloat16 t[3][4];
+    split3(x.x, t[0][0], t[1][0], t[2][0]);
+    split3(x.y, t[0][1], t[1][1], t[2][1]);
+    split3(x.z, t[0][2], t[1][2], t[2][2]);
+    split3(x.w, t[0][3], t[1][3], t[2][3]);
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) *reinterpret_cast<uint2*>(o + k * part_stride + i) = *reinterpret_cast<uint2*>(t[k]);
+  }
+}
+
+// One CTA per row; each thread owns 4-wide vectors (d % 4 == 0), kept in
+// registers between the residual add and the normalisation (d <= 8192).
 template <typename TD>
 __global__ void __launch_bounds__(256) add_rmsnorm_kernel(float* __restrict__ h, const TD* __restrict__ delta,
                                                           int n_parts, const float* __restrict__ gain, int rows,
                                                           int d, int mode, void* __restrict__ out) {
   __shared__ float red[8];
+  constexpr int kMaxVec = 8;  // 8 x 4 x 256 = 8192 elements per row
   const int r = blockIdx.x;
   float* hr = h + (int64_t)r * d;
   const int64_t pstride = (int64_t)rows * d;
+  float4 x[kMaxVec];
   float ss = 0.f;
-  for (int i = threadIdx.x; i < d; i += 256) {
-    float x = hr[i];
-    if (n_parts > 0) {
-      x += sum_parts(delta, n_parts, pstride, (int64_t)r * d + i);
-      hr[i] = x;
+#pragma unroll
+  for (int u = 0; u < kMaxVec; ++u) {
+    const int i = (u * 256 + threadIdx.x) * 4;
+    if (i < d) {
+      x[u] = ld4(hr + i);
+      if (n_parts > 0) {
+        for (int q = 0; q < n_parts; ++q) add4(x[u], ld4(delta + q * pstride + (int64_t)r * d + i));
+        *reinterpret_cast<float4*>(hr + i) = x[u];
+      }
+      ss += x[u].x * x[u].x + x[u].y * x[u].y + x[u].z * x[u].z + x[u].w * x[u].w;
     }
-    ss += x * x;
   }
   if (!out) return;
   float ms = block_sum_256(ss, red) / (float)d;
   float den = sqrtf(ms + 1e-6f);
-  for (int i = threadIdx.x; i < d; i += 256) {
-    store_mode(out, mode, pstride, (int64_t)r * d + i, hr[i] / den * gain[i]);
+#pragma unroll
+  for (int u = 0; u < kMaxVec; ++u) {
+    const int i = (u * 256 + threadIdx.x) * 4;
+    if (i < d) {
+      float4 g = ld4(gain + i);
+      float4 y = make_float4(x[u].x / den * g.x, x[u].y / den * g.y, x[u].z / den * g.z, x[u].w / den * g.w);
+      store4_mode(out, mode, pstride, (int64_t)r * d + i, y);
+    }
   }
 }
 
+__device__ __forceinline__ float silu_f(float g) {
+  if (g >= 0.f) return g / (1.f + expf(-g));
+  float e = expf(g);
+  return g * e / (1.f + e);
+}
+
+// 4-wide vectors over [rows][d_ff] (d_ff % 4 == 0).
 template <typename T>
 __global__ void silu_mul_kernel(const T* __restrict__ gu, int n_parts, int rows, int d_ff, int mode,
                                 void* __restrict__ out) {
-  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t n = (int64_t)rows * d_ff;
-  if (t >= n) return;
-  int64_t r = t / d_ff, c = t - r * d_ff;
+  const int vpr = d_ff / 4;
+  const int64_t nv = (int64_t)rows * vpr;
   const int64_t pstride = (int64_t)rows * 2 * d_ff;
-  float g = sum_parts(gu, n_parts, pstride, r * 2 * d_ff + c);
-  float u = sum_parts(gu, n_parts, pstride, r * 2 * d_ff + d_ff + c);
-  float s;
-  if (g >= 0.f) {
-    s = g / (1.f + expf(-g));
-  } else {
-    float e = expf(g);
-    s = g * e / (1.f + e);
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nv; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / vpr;
+    const int c = (int)(t - r * vpr) * 4;
+    const T* base = gu + r * 2 * d_ff + c;
+    float4 g = ld4(base), u = ld4(base + d_ff);
+    for (int q = 1; q < n_parts; ++q) {
+      add4(g, ld4(base + q * pstride));
+      add4(u, ld4(base + q * pstride + d_ff));
+    }
+    float4 y = make_float4(silu_f(g.x) * u.x, silu_f(g.y) * u.y, silu_f(g.z) * u.z, silu_f(g.w) * u.w);
+    store4_mode(out, mode, (int64_t)rows * d_ff, r * d_ff + c, y);
   }
-  store_mode(out, mode, n, t, s * u);
 }
 
 template <typename T>
@@ -109,7 +161,7 @@ using namespace ifkv;
 
 extern "C" int ifkv_add_rmsnorm(float* h, const void* delta, int delta_dtype, int n_parts, const float* gain,
                                 int rows, int d, int out_mode, void* out, void* stream) {
-  IFKV_CHECK_ARG(rows >= 0 && d > 0, "add_rmsnorm: bad shape");
+  IFKV_CHECK_ARG(rows >= 0 && d > 0 && d % 4 == 0 && d <= 8192, "add_rmsnorm: d must be a multiple of 4, <= 8192");
   IFKV_CHECK_ARG(out_mode >= IFKV_OUT_F32 && out_mode <= IFKV_OUT_SPLIT3, "add_rmsnorm: bad out mode");
   IFKV_CHECK_ARG(n_parts == 0 || delta_dtype == IFKV_F32 || delta_dtype == IFKV_BF16, "add_rmsnorm: bad dtype");
   if (rows == 0) return IFKV_OK;
@@ -125,11 +177,12 @@ extern "C" int ifkv_add_rmsnorm(float* h, const void* delta, int delta_dtype, in
 
 extern "C" int ifkv_silu_mul(const void* gu, int gu_dtype, int n_parts, int rows, int d_ff, int out_mode, void* out,
                              void* stream) {
-  IFKV_CHECK_ARG(rows >= 0 && d_ff > 0 && n_parts >= 1, "silu_mul: bad shape");
+  IFKV_CHECK_ARG(rows >= 0 && d_ff > 0 && d_ff % 4 == 0 && n_parts >= 1, "silu_mul: d_ff must be a multiple of 4");
   IFKV_CHECK_ARG(out_mode >= IFKV_OUT_F32 && out_mode <= IFKV_OUT_SPLIT3, "silu_mul: bad out mode");
-  int64_t n = (int64_t)rows * d_ff;
+  int64_t n = (int64_t)rows * d_ff / 4;
   if (n == 0) return IFKV_OK;
-  unsigned grid = (unsigned)((n + 255) / 256);
+  int64_t want = (n + 255) / 256;
+  unsigned grid = (unsigned)(want < 148 * 16 ? want : 148 * 16);
   if (gu_dtype == IFKV_BF16)
     silu_mul_kernel<__nv_bfloat16><<<grid, 256, 0, as_stream(stream)>>>((const __nv_bfloat16*)gu, n_parts, rows,
                                                                        d_ff, out_mode, out);

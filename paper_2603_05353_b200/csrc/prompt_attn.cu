@@ -121,21 +121,25 @@ __global__ void __launch_bounds__(256) prompt_attn_partial_kernel(
 }
 
 // grid (G * H * M), Dh threads (<= 256): merge the group's items in order.
+// Items of group g: [item_begin[g], item_begin[g+1]) then, if
+// prompt_item0 >= 0, item prompt_item0 + g (the group's causal prompt item).
 __global__ void prompt_attn_merge_kernel(const float* __restrict__ part_ml, const float* __restrict__ part_o,
-                                         const int32_t* __restrict__ item_begin, int H, int M, int Dh,
-                                         float* __restrict__ ctx, float* __restrict__ ml) {
+                                         const int32_t* __restrict__ item_begin, int prompt_item0, int H, int M,
+                                         int Dh, float* __restrict__ ctx, float* __restrict__ ml) {
   const int r = blockIdx.x;  // (g, h, m)
   const int m = r % M, h = (r / M) % H, g = r / (M * H);
   const int b = item_begin[g], e = item_begin[g + 1];
+  const int n = e - b + (prompt_item0 >= 0 ? 1 : 0);
+  auto item = [&](int k) { return k < e - b ? b + k : prompt_item0 + g; };
   float mx = -INFINITY;
-  for (int i = b; i < e; ++i) {
-    float mi = part_ml[2 * (((int64_t)i * H + h) * M + m)];
+  for (int k = 0; k < n; ++k) {
+    float mi = part_ml[2 * (((int64_t)item(k) * H + h) * M + m)];
     mx = fmaxf(mx, mi);
   }
   float l = 0.f, o = 0.f;
   const int d = threadIdx.x;
-  for (int i = b; i < e; ++i) {
-    int64_t row = ((int64_t)i * H + h) * M + m;
+  for (int k = 0; k < n; ++k) {
+    int64_t row = ((int64_t)item(k) * H + h) * M + m;
     float mi = part_ml[2 * row];
     if (mi == -INFINITY) continue;
     float a = expf(mi - mx);
@@ -214,12 +218,13 @@ extern "C" int ifkv_prompt_attn_partial(int kv_dtype, const float* qd, const voi
   return IFKV_OK;
 }
 
-extern "C" int ifkv_prompt_attn_merge(const float* part_ml, const float* part_o, const int32_t* item_begin, int G,
-                                      int H, int M, int Dh, float* ctx, float* ml, void* stream) {
+extern "C" int ifkv_prompt_attn_merge(const float* part_ml, const float* part_o, const int32_t* item_begin,
+                                      int prompt_item0, int G, int H, int M, int Dh, float* ctx, float* ml,
+                                      void* stream) {
   IFKV_CHECK_ARG(Dh <= 256 && G > 0, "prompt_attn_merge: bad shape");
   int threads = ((Dh + 31) / 32) * 32;
-  prompt_attn_merge_kernel<<<G * H * M, threads, 0, as_stream(stream)>>>(part_ml, part_o, item_begin, H, M, Dh, ctx,
-                                                                          ml);
+  prompt_attn_merge_kernel<<<G * H * M, threads, 0, as_stream(stream)>>>(part_ml, part_o, item_begin, prompt_item0,
+                                                                          H, M, Dh, ctx, ml);
   IFKV_LAUNCH_CHECK("prompt_attn_merge");
   return IFKV_OK;
 }

@@ -80,7 +80,8 @@ __global__ void __launch_bounds__(256) rotate_rows_kernel(const T* __restrict__ 
 // Rotated query sets: qd[s][h][m][:] = R(-angle) q[g][m][h][:].
 __global__ void rotate_queries_kernel(const float* __restrict__ q, int M, int H, int Dh,
                                       const int32_t* __restrict__ qset_group, const int32_t* __restrict__ qset_cs,
-                                      int n_qsets, const float2* __restrict__ cs, float* __restrict__ qd) {
+                                      int n_qsets, const float2* __restrict__ cs, float* __restrict__ qd,
+                                      __nv_bfloat16* __restrict__ qd3) {
   int half = Dh / 2;
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t total = (int64_t)n_qsets * H * M * half;
@@ -101,9 +102,22 @@ __global__ void rotate_queries_kernel(const float* __restrict__ q, int M, int H,
     y0 = x0 * c.x + x1 * c.y;   // rotation by -angle
     y1 = -x0 * c.y + x1 * c.x;
   }
-  float* d = qd + (((int64_t)s * H + h) * M + m) * Dh + 2 * p;
-  d[0] = y0;
-  d[1] = y1;
+  const int64_t o = (((int64_t)s * H + h) * M + m) * Dh + 2 * p;
+  qd[o] = y0;
+  qd[o + 1] = y1;
+  if (qd3) {  // [n_qsets][3][H][M][Dh] split terms for the tensor-core scorer
+    const int64_t plane = (int64_t)H * M * Dh;
+    const int64_t o3 = ((int64_t)s * 3) * plane + (o - (int64_t)s * plane);
+    __nv_bfloat16 a0, a1, a2, b0, b1, b2;
+    split3(y0, a0, a1, a2);
+    split3(y1, b0, b1, b2);
+    qd3[o3] = a0;
+    qd3[o3 + 1] = b0;
+    qd3[o3 + plane] = a1;
+    qd3[o3 + plane + 1] = b1;
+    qd3[o3 + 2 * plane] = a2;
+    qd3[o3 + 2 * plane + 1] = b2;
+  }
 }
 
 // Fresh q/k/v epilogue: rope q and k at the rows' positions, write q
@@ -145,6 +159,50 @@ __global__ void qkv_rope_scatter_kernel(const TIn* __restrict__ qkv, int n_parts
   }
   d[0] = from_f32<TOut>(x0);
   d[1] = from_f32<TOut>(x1);
+}
+
+// Vectorised variant (Dh % 8 == 0): one thread = 8 consecutive elements
+// (4 pairs) of one head row.
+template <typename TIn, typename TOut>
+__global__ void qkv_rope_scatter_vec_kernel(const TIn* __restrict__ qkv, int n_parts, int64_t part_stride, int rows,
+                                            int H, int Hkv, int Dh, const float2* __restrict__ cs,
+                                            TOut* __restrict__ q_out, TOut* __restrict__ k_dst,
+                                            TOut* __restrict__ v_dst, const int64_t* __restrict__ dst_rows) {
+  const int half = Dh / 2;
+  const int vpr = (H + 2 * Hkv) * Dh / 8;  // vectors per row
+  const int64_t total = (int64_t)rows * vpr;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(t / vpr);
+    const int c8 = (int)(t - (int64_t)r * vpr) * 8;  // element column
+    const int head = c8 / Dh, e0 = c8 % Dh;
+    if (head < H && !q_out) continue;
+    float x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = 0.f;
+    const TIn* src = qkv + (int64_t)r * (H + 2 * Hkv) * Dh + c8;
+    for (int p = 0; p < n_parts; ++p) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] += to_f32(src[p * part_stride + u]);
+    }
+    if (head < H + Hkv) {
+      const float2* c = cs + (int64_t)r * half + e0 / 2;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        float2 a = c[u];
+        float y0 = x[2 * u] * a.x - x[2 * u + 1] * a.y;
+        float y1 = x[2 * u] * a.y + x[2 * u + 1] * a.x;
+        x[2 * u] = y0;
+        x[2 * u + 1] = y1;
+      }
+    }
+    const int64_t drow = dst_rows ? dst_rows[r] : r;
+    TOut* d;
+    if (head < H) d = q_out + ((int64_t)r * H + head) * Dh + e0;
+    else if (head < H + Hkv) d = k_dst + (drow * Hkv + (head - H)) * Dh + e0;
+    else d = v_dst + (drow * Hkv + (head - H - Hkv)) * Dh + e0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) d[u] = from_f32<TOut>(x[u]);
+  }
 }
 
 }  // namespace ifkv
@@ -199,12 +257,14 @@ extern "C" int ifkv_rotate_rows(int dtype, const void* src, void* dst, int64_t l
 }
 
 extern "C" int ifkv_rotate_queries(const float* q, int G, int M, int H, int Dh, const int32_t* qset_group,
-                                   const int32_t* qset_cs, int n_qsets, const float* cs, float* qd, void* stream) {
+                                   const int32_t* qset_cs, int n_qsets, const float* cs, float* qd, void* qd3,
+                                   void* stream) {
   IFKV_CHECK_ARG(Dh % 2 == 0 && G > 0 && M > 0 && H > 0, "rotate_queries: bad shape");
   if (n_qsets <= 0) return IFKV_OK;
   int64_t total = (int64_t)n_qsets * H * M * (Dh / 2);
   rotate_queries_kernel<<<(unsigned)((total + 255) / 256), 256, 0, as_stream(stream)>>>(
-      q, M, H, Dh, qset_group, qset_cs, n_qsets, reinterpret_cast<const float2*>(cs), qd);
+      q, M, H, Dh, qset_group, qset_cs, n_qsets, reinterpret_cast<const float2*>(cs), qd,
+      reinterpret_cast<__nv_bfloat16*>(qd3));
   IFKV_LAUNCH_CHECK("rotate_queries");
   return IFKV_OK;
 }
@@ -221,9 +281,19 @@ extern "C" int ifkv_qkv_rope_scatter(const void* qkv, int qkv_dtype, int n_parts
   unsigned grid = (unsigned)((total + 255) / 256);
   auto c = reinterpret_cast<const float2*>(cs);
   cudaStream_t s = as_stream(stream);
-#define IFKV_QKV_LAUNCH(TI, TO)                                                                                \
-  qkv_rope_scatter_kernel<TI, TO><<<grid, 256, 0, s>>>((const TI*)qkv, n_parts, part_stride, rows, H, Hkv, Dh, c, \
-                                                       (TO*)q_out, (TO*)k_dst, (TO*)v_dst, dst_rows)
+  const bool vec = Dh % 8 == 0;
+  if (vec) {
+    int64_t nv = (int64_t)rows * (H + 2 * Hkv) * Dh / 8;
+    int64_t want = (nv + 255) / 256;
+    grid = (unsigned)(want < 148 * 16 ? want : 148 * 16);
+  }
+#define IFKV_QKV_LAUNCH(TI, TO)                                                                                   \
+  if (vec)                                                                                                        \
+    qkv_rope_scatter_vec_kernel<TI, TO><<<grid, 256, 0, s>>>((const TI*)qkv, n_parts, part_stride, rows, H, Hkv,   \
+                                                             Dh, c, (TO*)q_out, (TO*)k_dst, (TO*)v_dst, dst_rows); \
+  else                                                                                                            \
+    qkv_rope_scatter_kernel<TI, TO><<<grid, 256, 0, s>>>((const TI*)qkv, n_parts, part_stride, rows, H, Hkv, Dh, c, \
+                                                         (TO*)q_out, (TO*)k_dst, (TO*)v_dst, dst_rows)
   if (qkv_dtype == IFKV_F32 && out_dtype == IFKV_F32) IFKV_QKV_LAUNCH(float, float);
   else if (qkv_dtype == IFKV_F32) IFKV_QKV_LAUNCH(float, __nv_bfloat16);
   else if (out_dtype == IFKV_F32) IFKV_QKV_LAUNCH(__nv_bfloat16, float);

@@ -184,3 +184,21 @@ int make_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t*
                    const uint32_t* box);
 
 }  // namespace ifkv
+
+namespace ifkv {
+namespace tc {
+// D[tmem] (+)= A[tmem] * B[smem]: A (M x K bf16) lives in TMEM, lane = row,
+// 2 bf16 per 32-bit column (low half = even k).
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+}  // namespace tc
+}  // namespace ifkv

@@ -263,7 +263,10 @@ def segments_from_deltas(deltas: np.ndarray, row_offset: int = 0) -> List[Tuple[
 
 
 def _plan_items(groups: Sequence[PromptGroup], M: int):
-    """Work items (24-byte ifkv_attn_item rows), query sets and deltas."""
+    """Work items (24-byte ifkv_attn_item rows): every group's context items
+    (<= ITEM_KEYS keys of one constant-delta run), groups in order, then one
+    causal prompt item per group.  Returns (items, ctx_begin [G+1], n_ctx,
+    qset_group, qset_cs, deltas)."""
     deltas = sorted({d for g in groups for (_, _, d) in g.segments if d != 0})
     delta_id = {d: i for i, d in enumerate(deltas)}
     qset_group, qset_cs, qset_of = [], [], {}
@@ -276,22 +279,26 @@ def _plan_items(groups: Sequence[PromptGroup], M: int):
             qset_cs.append(delta_id[d] if d != 0 else -1)
         return qset_of[key]
 
-    items, item_begin = [], [0]
+    items, ctx_begin = [], [0]
     for gi, g in enumerate(groups):
         for row0, n, d in g.segments:
             qs = qset(gi, d)
             for off in range(0, n, ITEM_KEYS):
                 items.append((gi, qs, row0 + off, min(ITEM_KEYS, n - off), 0, 1))
+        ctx_begin.append(len(items))
+    n_ctx = len(items)
+    for gi in range(len(groups)):
         items.append((gi, qset(gi, 0), 0, M, 1, 0))
-        item_begin.append(len(items))
-    return (np.asarray(items, dtype=np.int32).reshape(-1, 6), np.asarray(item_begin, np.int32),
+    return (np.asarray(items, dtype=np.int32).reshape(-1, 6), np.asarray(ctx_begin, np.int32), n_ctx,
             np.asarray(qset_group, np.int32), np.asarray(qset_cs, np.int32), deltas)
 
 
 def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], capture_layer: Optional[int] = None,
-                   want_logits: bool = False) -> PromptOut:
+                   want_logits: bool = False, impl: str = "auto") -> PromptOut:
     """Run every group's prompt forward; capture column scores at
-    ``capture_layer`` (then stop) or return last-row logits."""
+    ``capture_layer`` (then stop) or return last-row logits.  impl "auto"
+    uses the tcgen05 kernels for bf16 slabs with Dh = 128, "simt" forces the
+    generic kernels."""
     torch = _torch()
     cfg = weights.config
     dev = weights.device
@@ -302,50 +309,73 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
         raise ConfigurationError("all prompt groups must have the same length")
     bf16 = weights.precision == "bf16"
     mode = N.OUT_SPLIT3 if bf16 else N.OUT_F32
-    items_np, item_begin_np, qg_np, qc_np, deltas = _plan_items(groups, M)
+    kv_dt = dt_code(slab_k)
+    use_tc = impl == "auto" and bool(N.call("ifkv_prompt_attn_tc_supported", kv_dt, H, Hkv, M, Dh))
+    items_np, ctx_begin_np, n_ctx, qg_np, qc_np, deltas = _plan_items(groups, M)
     n_items, n_qsets = items_np.shape[0], qg_np.size
-    meta = torch.as_tensor(np.concatenate([items_np.ravel(), item_begin_np, qg_np, qc_np]), device=dev)
+    meta = torch.as_tensor(np.concatenate([items_np.ravel(), ctx_begin_np, qg_np, qc_np]), device=dev)
     items_p = meta.data_ptr()
+    prompt_items_p = items_p + 24 * n_ctx
     ib_p = items_p + 4 * items_np.size
-    qg_p = ib_p + 4 * item_begin_np.size
+    qg_p = ib_p + 4 * ctx_begin_np.size
     qc_p = qg_p + 4 * qg_np.size
     cs_delta = rope_table(np.asarray(deltas, np.int64) if deltas else np.zeros(1, np.int64), Dh, cfg.rope_base, dev)
     ids = torch.as_tensor(np.concatenate([np.asarray(g.token_ids, np.int64) for g in groups]), device=dev)
-    cs_prompt = rope_table(np.concatenate([np.asarray(g.positions, np.int64) for g in groups]), Dh, cfg.rope_base, dev)
     pos_all = np.concatenate([np.asarray(g.positions, np.int64) for g in groups])
     if pos_all.min() < 0 or pos_all.max() >= cfg.max_position:
         raise ConfigurationError(f"position outside [0, {cfg.max_position}): {int(pos_all.max())}")
     if capture_layer is not None and not 0 <= capture_layer < cfg.n_layers:
         raise ConfigurationError(f"capture layer {capture_layer} outside [0, {cfg.n_layers})")
+    cs_prompt = rope_table(pos_all, Dh, cfg.rope_base, dev)
     rows = G * M
+    n_rows = slab_k.shape[1]
     h = embed_rows(weights.embedding, ids)
     q = torch.empty((rows, H, Dh), dtype=torch.float32, device=dev)
     kp = torch.empty((rows, Hkv, Dh), dtype=torch.float32, device=dev)
     vp = torch.empty_like(kp)
     qd = torch.empty((n_qsets, H, M, Dh), dtype=torch.float32, device=dev)
+    qd3 = torch.empty((n_qsets, 3, H, M, Dh), dtype=torch.bfloat16, device=dev) if use_tc else None
     part_ml = torch.empty((n_items, H, M, 2), dtype=torch.float32, device=dev)
     part_o = torch.empty((n_items, H, M, Dh), dtype=torch.float32, device=dev)
     ctx = torch.empty((G, M, H, Dh), dtype=torch.float32, device=dev)
     ml = torch.empty((G, H, M, 2), dtype=torch.float32, device=dev)
     scale = 1.0 / math.sqrt(Dh)
-    kv_dt = dt_code(slab_k)
     pending, pending_parts = None, 0
     last = cfg.n_layers - 1 if capture_layer is None else capture_layer
     out = PromptOut()
+    stride_ml, stride_o = H * M * 2 * 4, H * M * Dh * 4
     for li in range(last + 1):
         lw = weights.layers[li]
         x = add_rmsnorm(h, pending, pending_parts, lw.attn_norm, mode)
         qkv = mm_parts(x, lw.wqkv)
         qkv_rope_scatter(qkv, qkv.shape[0], H, Hkv, Dh, cs_prompt, q, kp, vp, None)
-        N.call("ifkv_rotate_queries", N.ptr(q), G, M, H, Dh, qg_p, qc_p, n_qsets, N.ptr(cs_delta), N.ptr(qd), _s())
-        N.call("ifkv_prompt_attn_partial", kv_dt, N.ptr(qd), N.ptr(slab_k[li]), N.ptr(slab_v[li]), N.ptr(kp),
-               N.ptr(vp), items_p, n_items, H, Hkv, M, Dh, scale, N.ptr(part_ml), N.ptr(part_o), _s())
-        N.call("ifkv_prompt_attn_merge", N.ptr(part_ml), N.ptr(part_o), ib_p, G, H, M, Dh, N.ptr(ctx), N.ptr(ml),
-               _s())
-        if capture_layer is not None and li == capture_layer:
-            scores = torch.zeros(slab_k.shape[1], dtype=torch.float32, device=dev)
-            N.call("ifkv_score_columns", kv_dt, N.ptr(qd), N.ptr(slab_k[li]), items_p, n_items, N.ptr(ml), H, Hkv,
-                   M, Dh, scale, N.ptr(scores), _s())
+        N.call("ifkv_rotate_queries", N.ptr(q), G, M, H, Dh, qg_p, qc_p, n_qsets, N.ptr(cs_delta), N.ptr(qd),
+               N.ptr(qd3), _s())
+        capture = capture_layer is not None and li == capture_layer
+        with _Bracket("prompt_attn", li):
+            if use_tc:
+                N.call("ifkv_prompt_attn_partial_tc", N.ptr(qd3), n_qsets, N.ptr(slab_k[li]), N.ptr(slab_v[li]),
+                       n_rows, items_p, n_ctx, H, Hkv, M, scale, N.ptr(part_ml), N.ptr(part_o), _s())
+                N.call("ifkv_prompt_attn_partial", kv_dt, N.ptr(qd), N.ptr(slab_k[li]), N.ptr(slab_v[li]), N.ptr(kp),
+                       N.ptr(vp), prompt_items_p, n_items - n_ctx, H, Hkv, M, Dh, scale,
+                       part_ml.data_ptr() + n_ctx * stride_ml, part_o.data_ptr() + n_ctx * stride_o, _s())
+            else:
+                N.call("ifkv_prompt_attn_partial", kv_dt, N.ptr(qd), N.ptr(slab_k[li]), N.ptr(slab_v[li]), N.ptr(kp),
+                       N.ptr(vp), items_p, n_items, H, Hkv, M, Dh, scale, N.ptr(part_ml), N.ptr(part_o), _s())
+            N.call("ifkv_prompt_attn_merge", N.ptr(part_ml), N.ptr(part_o), ib_p, n_ctx, G, H, M, Dh, N.ptr(ctx),
+                   N.ptr(ml), _s())
+        if capture:
+            scores = torch.zeros(n_rows, dtype=torch.float32, device=dev)
+            with _Bracket("score_columns", li):
+                if use_tc:
+                    hpt = min(128 // M, H // Hkv)
+                    n_chunks = Hkv * (-(-(H // Hkv) // hpt))
+                    ws = torch.empty((n_ctx, n_chunks, 128), dtype=torch.float32, device=dev)
+                    N.call("ifkv_score_columns_tc", N.ptr(qd3), n_qsets, N.ptr(slab_k[li]), n_rows, items_p, n_ctx,
+                           N.ptr(ml), H, Hkv, M, scale, N.ptr(ws), N.ptr(scores), _s())
+                else:
+                    N.call("ifkv_score_columns", kv_dt, N.ptr(qd), N.ptr(slab_k[li]), items_p, n_ctx, N.ptr(ml), H,
+                           Hkv, M, Dh, scale, N.ptr(scores), _s())
             out.scores, out.ml = scores, ml
             return out
         cx = split3(ctx.view(rows, d)) if bf16 else ctx.view(rows, d)

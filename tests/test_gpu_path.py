@@ -207,3 +207,31 @@ def test_gqa_path_vs_oracle(cuda, precision):
     gk, gv = P.decode_view(out, cfg.rope_base)
     tol = 1e-2 if precision == "bf16" else 1e-4
     assert rel_err(to_np(gk), wk) <= tol and rel_err(to_np(gv), wv) <= tol
+
+
+def test_tc_scorer_gqa_dh128_vs_simt_and_oracle(cuda):
+    """tcgen05 scorer (G = 4 heads x 32 prompt rows = 128-row tiles, ragged
+    192-row chunks -> partial key items) vs the SIMT scorer and the oracle."""
+    P = _pkg()
+    from paper_2603_05353_b200 import engine as E
+
+    cfg = P.ModelConfig(n_layers=3, n_heads=8, d_model=1024, d_head=128, d_ff=512, vocab_size=256,
+                        max_position=8192, n_kv_heads=2)
+    dw, ow, _ = _setup(cfg, 5, "bf16", None, None)
+    rng = np.random.default_rng(9)
+    toks, prompt = rng.integers(0, 256, 768), rng.integers(0, 256, 32)
+    chunks = P.make_chunks(toks, [192] * 4)
+    kvs = [P.prefill_chunk(dw, c) for c in chunks]
+    cache = P.assemble(kvs)
+    geo = P.GeometryConfig(mode="global", prompt_length=32, chunk_lengths=(192,) * 4)
+    a = P.assign_positions(geo, chunks)
+    grp = E.PromptGroup(prompt, a.prompt_positions, E.segments_from_deltas(a.context_concat() - cache.row_positions))
+    tc = E.prompt_forward(dw, cache.keys, cache.values, [grp], capture_layer=2).scores[:768].double().cpu().numpy()
+    simt = E.prompt_forward(dw, cache.keys, cache.values, [grp], capture_layer=2,
+                            impl="simt").scores[:768].double().cpu().numpy()
+    oc = O.assemble([oracle_chunk(c) for c in kvs])
+    s, sel = O.run_selection(ow, oc, prompt, ratio=0.15, norm_layer=2)
+    assert rel_err(tc, s) <= 1e-5 and rel_err(simt, s) <= 1e-5
+    np.testing.assert_array_equal(P.select_topk(tc, sel.size).cpu().numpy(), sel)
+    res = P.run_selection(dw, chunks, cache, prompt, P.SelectionConfig(ratio=0.15, norm_layer=2))
+    np.testing.assert_array_equal(res.selected_numpy(), sel)

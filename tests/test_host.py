@@ -83,12 +83,13 @@ def test_segments_and_work_items():
     assert E.segments_from_deltas(d, 10) == [(10, 2, 0), (12, 3, 5), (15, 1, 0), (16, 1, 9)]
     g = [E.PromptGroup(np.arange(4), np.arange(4), [(0, 300, 7), (300, 10, 0)]),
          E.PromptGroup(np.arange(4), np.arange(4), [(310, 5, 7)])]
-    items, begin, qg, qc, deltas = E._plan_items(g, 4)
+    items, begin, n_ctx, qg, qc, deltas = E._plan_items(g, 4)
     assert deltas == [7]
-    assert begin.tolist() == [0, 5, 7]
-    # group 0: 300 rows -> 3 items of <=128 keys, 1 item of 10 rows, prompt item
-    assert items[:, 3].tolist() == [128, 128, 44, 10, 4, 5, 4]
-    assert items[:, 4].tolist() == [0, 0, 0, 0, 1, 0, 1]
+    # context items first (group 0: 300 rows -> 128, 128, 44; then 10 rows; group 1: 5), then one prompt item per group
+    assert begin.tolist() == [0, 4, 5] and n_ctx == 5
+    assert items[:, 3].tolist() == [128, 128, 44, 10, 5, 4, 4]
+    assert items[:, 4].tolist() == [0, 0, 0, 0, 0, 1, 1]
+    assert items[:, 0].tolist() == [0, 0, 0, 0, 1, 0, 1]
     assert qg.tolist() == [0, 0, 1, 1] and qc.tolist() == [0, -1, 0, -1]
 
 
