@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(256, 1)
     const int row = w * 32 + lane;
     const int tok = t0 + row / G;
     const bool valid = tok < S;
-    const int64_t hz = valid ? horizon[tok] : 0;
+    const int hz = valid ? (int)horizon[tok] : 0;
     const uint32_t lane_off = (uint32_t)(w * 32) << 16;
     float m_used = -INFINITY, l = 0.f;
     float v[kKeys];
@@ -167,13 +167,16 @@ __global__ void __launch_bounds__(256, 1)
       tc::tmem_ld_wait();
       tc::tc_fence_before();
       tc::mbar_arrive(&sm.s_free[s]);
-      const int64_t j0 = (int64_t)j * kKeys;
+      const int j0 = j * kKeys;
+      // causal mask only where the block crosses this warp's horizons
+      if (__any_sync(0xffffffffu, j0 + kKeys - 1 > hz)) {
+#pragma unroll
+        for (int c = 0; c < kKeys; ++c)
+          if (j0 + c > hz) v[c] = -INFINITY;
+      }
       float mx = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < kKeys; ++c) {
-        if (j0 + c > hz) v[c] = -INFINITY;
-        mx = fmaxf(mx, v[c]);
-      }
+      for (int c = 0; c < kKeys; c += 2) mx = tc::max3(mx, v[c], v[c + 1]);
       float alpha = 1.f;
       bool need = false;
       if (mx > -INFINITY && (m_used == -INFINITY || (mx - m_used) * scale_log2 > kRescaleLog2)) {
@@ -191,8 +194,7 @@ __global__ void __launch_bounds__(256, 1)
         float e[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          float x = v[ch * 8 + u];
-          e[u] = x == -INFINITY ? 0.f : tc::ex2(fmaf(x, scale_log2, -mb));
+          e[u] = tc::ex2(fmaf(v[ch * 8 + u], scale_log2, -mb));  // ex2.approx.ftz(-inf) = +0
           sum += e[u];
         }
         uint4 pk;
