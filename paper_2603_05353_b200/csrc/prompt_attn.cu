@@ -42,8 +42,9 @@ __device__ void stage_item(const ifkv_attn_item& it, int kv_dtype, const void* k
   }
 }
 
-// grid (n_items, Hkv), 256 threads.  Warp w handles query rows w, w+8, ...
-// of the item's group restricted to kv head g (grp heads x M rows).
+// grid (n_items, Hkv, row_splits), 256 threads.  Warp w of split z handles
+// query rows 8z + w, 8z + w + 8*row_splits, ... of the item's group restricted
+// to kv head g (grp heads x M rows).
 __global__ void __launch_bounds__(256) prompt_attn_partial_kernel(
     int kv_dtype, const float* __restrict__ qd, const void* __restrict__ k_slab, const void* __restrict__ v_slab,
     const float* __restrict__ k_prompt, const float* __restrict__ v_prompt, const ifkv_attn_item* __restrict__ items,
@@ -61,7 +62,7 @@ __global__ void __launch_bounds__(256) prompt_attn_partial_kernel(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* q = Qs + warp * Dh;
   const int rows = grp * M;
-  for (int r = warp; r < rows; r += 8) {
+  for (int r = blockIdx.z * 8 + warp; r < rows; r += 8 * gridDim.z) {
     const int h = g * grp + r / M, m = r % M;
     const float* qsrc = qd + (((int64_t)it.qset * H + h) * M + m) * Dh;
     for (int d = lane; d < Dh; d += 32) q[d] = qsrc[d];
@@ -210,7 +211,11 @@ extern "C" int ifkv_prompt_attn_partial(int kv_dtype, const float* qd, const voi
   IFKV_CUDA_CALL(cudaFuncSetAttribute(prompt_attn_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)sm),
                  "prompt_attn_partial: smem attribute");
-  dim3 grid(n_items, Hkv);
+  const int rows = (H / Hkv) * M;
+  int splits = (rows + 7) / 8;
+  const int64_t ctas = (int64_t)n_items * Hkv;
+  while (splits > 1 && ctas * splits > 4 * 148) splits = (splits + 1) / 2;  // enough CTAs, bounded restaging
+  dim3 grid(n_items, Hkv, splits);
   prompt_attn_partial_kernel<<<grid, 256, sm, as_stream(stream)>>>(kv_dtype, qd, k_slab, v_slab, k_prompt,
                                                                      v_prompt, items, H, Hkv, M, Dh, scale, part_ml,
                                                                      part_o);
