@@ -116,7 +116,7 @@ typedef struct {
   int32_t group;    /* query group                                          */
   int32_t qset;     /* rotated query set (qd index)                         */
   int32_t key_row0; /* first key row (slab row, or prompt row 0)            */
-  int32_t n_keys;   /* number of keys, 1..128                               */
+  int32_t n_keys;   /* number of keys (<= 128 for the SIMT kernels)         */
   int32_t prompt;   /* 1: keys are the group's prompt rows, causal          */
   int32_t score;    /* 1: context item whose columns are scored             */
 } ifkv_attn_item;
@@ -146,16 +146,18 @@ int ifkv_rotate_queries(const float* q, int G, int M, int H, int Dh, const int32
 /* Tensor-core (tcgen05/TMEM/TMA) versions for bf16 slabs with Dh = 128:
  * S = sum_t Q_t K^T and O = sum_t P_t V over hi/mid/lo bf16 terms of the fp32
  * queries / probabilities (exact products, fp32 sums), one CTA per (context
- * item, kv head, <=128-row head chunk).  Context items only (prompt items go
- * to the SIMT kernel).  n_rows = rows of the slab layer view. */
+ * item, kv head, <=128-row head chunk); an item may span several 128-key
+ * blocks (n_keys <= item_keys, a multiple of 128), streamed through a TMA
+ * ring with an online softmax.  Context items only (prompt items go to the
+ * SIMT kernel).  n_rows = rows of the slab layer view. */
 int ifkv_prompt_attn_tc_supported(int kv_dtype, int H, int Hkv, int M, int Dh);
 int ifkv_prompt_attn_partial_tc(const void* qd3, int n_qsets, const void* k_slab, const void* v_slab, int n_rows,
-                                const ifkv_attn_item* items, int n_items, int H, int Hkv, int M, float scale,
-                                float* part_ml, float* part_o, void* stream);
-/* colsum_ws: fp32 [n_items][Hkv * head_chunks][128] workspace. */
+                                const ifkv_attn_item* items, int n_items, int item_keys, int H, int Hkv, int M,
+                                float scale, float* part_ml, float* part_o, void* stream);
+/* colsum_ws: fp32 [n_items][Hkv * head_chunks][item_keys] workspace. */
 int ifkv_score_columns_tc(const void* qd3, int n_qsets, const void* k_slab, int n_rows, const ifkv_attn_item* items,
-                          int n_items, const float* ml, int H, int Hkv, int M, float scale, float* colsum_ws,
-                          float* scores, void* stream);
+                          int n_items, int item_keys, const float* ml, int H, int Hkv, int M, float scale,
+                          float* colsum_ws, float* scores, void* stream);
 
 /* ---- top-k (selection.py:172-183) and per-chunk importance
  * (reorder.py:84-112) -----------------------------------------------------

@@ -262,7 +262,7 @@ def segments_from_deltas(deltas: np.ndarray, row_offset: int = 0) -> List[Tuple[
     return [(row_offset + int(a), int(b - a), int(deltas[a])) for a, b in zip(starts, ends)]
 
 
-def _plan_items(groups: Sequence[PromptGroup], M: int):
+def _plan_items(groups: Sequence[PromptGroup], M: int, item_keys: int = ITEM_KEYS):
     """Work items (24-byte ifkv_attn_item rows): every group's context items
     (<= ITEM_KEYS keys of one constant-delta run), groups in order, then one
     causal prompt item per group.  Returns (items, ctx_begin [G+1], n_ctx,
@@ -283,14 +283,30 @@ def _plan_items(groups: Sequence[PromptGroup], M: int):
     for gi, g in enumerate(groups):
         for row0, n, d in g.segments:
             qs = qset(gi, d)
-            for off in range(0, n, ITEM_KEYS):
-                items.append((gi, qs, row0 + off, min(ITEM_KEYS, n - off), 0, 1))
+            for off in range(0, n, item_keys):
+                items.append((gi, qs, row0 + off, min(item_keys, n - off), 0, 1))
         ctx_begin.append(len(items))
     n_ctx = len(items)
     for gi in range(len(groups)):
         items.append((gi, qset(gi, 0), 0, M, 1, 0))
     return (np.asarray(items, dtype=np.int32).reshape(-1, 6), np.asarray(ctx_begin, np.int32), n_ctx,
             np.asarray(qset_group, np.int32), np.asarray(qset_cs, np.int32), deltas)
+
+
+def _tc_item_keys(groups, Hkv: int, G: int, M: int, sms: int = 148) -> int:
+    """Keys per tensor-core work item: the longest multiple of 128 (<= 16
+    blocks) that still gives >= 2 CTAs per SM; fewer, longer items mean fewer
+    (m, l, O) partials to write and merge."""
+    hpt = max(1, min(128 // M, G))
+    chunks = Hkv * (-(-G // hpt))
+    runs = [n for g in groups for (_, n, _) in g.segments]
+    best = 128
+    for ipc in (2, 4, 8, 16):
+        ctas = chunks * sum(-(-n // (128 * ipc)) for n in runs)
+        if ctas < 2 * sms:
+            break
+        best = 128 * ipc
+    return best
 
 
 def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], capture_layer: Optional[int] = None,
@@ -311,7 +327,8 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
     mode = N.OUT_SPLIT3 if bf16 else N.OUT_F32
     kv_dt = dt_code(slab_k)
     use_tc = impl == "auto" and bool(N.call("ifkv_prompt_attn_tc_supported", kv_dt, H, Hkv, M, Dh))
-    items_np, ctx_begin_np, n_ctx, qg_np, qc_np, deltas = _plan_items(groups, M)
+    item_keys = _tc_item_keys(groups, Hkv, H // Hkv, M) if use_tc else ITEM_KEYS
+    items_np, ctx_begin_np, n_ctx, qg_np, qc_np, deltas = _plan_items(groups, M, item_keys)
     n_items, n_qsets = items_np.shape[0], qg_np.size
     meta = torch.as_tensor(np.concatenate([items_np.ravel(), ctx_begin_np, qg_np, qc_np]), device=dev)
     items_p = meta.data_ptr()
@@ -355,7 +372,7 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
         with _Bracket("prompt_attn", li):
             if use_tc:
                 N.call("ifkv_prompt_attn_partial_tc", N.ptr(qd3), n_qsets, N.ptr(slab_k[li]), N.ptr(slab_v[li]),
-                       n_rows, items_p, n_ctx, H, Hkv, M, scale, N.ptr(part_ml), N.ptr(part_o), _s())
+                       n_rows, items_p, n_ctx, item_keys, H, Hkv, M, scale, N.ptr(part_ml), N.ptr(part_o), _s())
                 N.call("ifkv_prompt_attn_partial", kv_dt, N.ptr(qd), N.ptr(slab_k[li]), N.ptr(slab_v[li]), N.ptr(kp),
                        N.ptr(vp), prompt_items_p, n_items - n_ctx, H, Hkv, M, Dh, scale,
                        part_ml.data_ptr() + n_ctx * stride_ml, part_o.data_ptr() + n_ctx * stride_o, _s())
@@ -370,9 +387,9 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
                 if use_tc:
                     hpt = min(128 // M, H // Hkv)
                     n_chunks = Hkv * (-(-(H // Hkv) // hpt))
-                    ws = torch.empty((n_ctx, n_chunks, 128), dtype=torch.float32, device=dev)
+                    ws = torch.empty((n_ctx, n_chunks, item_keys), dtype=torch.float32, device=dev)
                     N.call("ifkv_score_columns_tc", N.ptr(qd3), n_qsets, N.ptr(slab_k[li]), n_rows, items_p, n_ctx,
-                           N.ptr(ml), H, Hkv, M, scale, N.ptr(ws), N.ptr(scores), _s())
+                           item_keys, N.ptr(ml), H, Hkv, M, scale, N.ptr(ws), N.ptr(scores), _s())
                 else:
                     N.call("ifkv_score_columns", kv_dt, N.ptr(qd), N.ptr(slab_k[li]), items_p, n_ctx, N.ptr(ml), H,
                            Hkv, M, Dh, scale, N.ptr(scores), _s())
