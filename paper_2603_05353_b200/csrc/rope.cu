@@ -20,60 +20,101 @@ __global__ void rope_table_kernel(const int64_t* __restrict__ pos, int n, int ha
 }
 
 // ---- Kernel 1 -----------------------------------------------------------
-// One thread moves one 16-byte vector (8 bf16 / 4 fp32 = 4 / 2 pairs) and
-// handles kUnroll vectors with all loads issued before any store.  Rows whose
-// table entry is negative are skipped (in place) or copied bit-exactly.
-template <typename T, int kUnroll>
+// One warp per (layer, row) pair, two rows in flight per warp: every lane
+// issues all its 16-byte loads (8 bf16 / 4 fp32 = 4 / 2 RoPE pairs per
+// vector) before rotating and storing.  The row's cos/sin come from a small
+// fp64-derived table (one entry per distinct delta) that stays in L1.  Rows
+// whose table entry is negative (delta 0) are skipped in place or copied
+// bit-exactly out of place.
+template <typename T, int kVpl>
 __global__ void __launch_bounds__(256) rotate_rows_kernel(const T* __restrict__ src, T* __restrict__ dst,
-                                                          int64_t layer_stride, int64_t n_rows,
-                                                          int vecs_per_row, int vecs_per_head,
-                                                          int64_t total_vecs, const int32_t* __restrict__ row_table,
+                                                          int64_t layer_stride, int n_rows, int n_layers,
+                                                          int vecs_per_head, const int32_t* __restrict__ row_table,
                                                           const float2* __restrict__ cs, int half, bool in_place) {
   constexpr int kVec = 16 / sizeof(T);
   constexpr int kPairs = kVec / 2;
-  using V = uint4;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; base < total_vecs;
-       base += stride * kUnroll) {
-    V val[kUnroll];
-    int tab[kUnroll];
-    bool live[kUnroll];
-    int64_t off[kUnroll];
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  const int64_t total = (int64_t)n_layers * n_rows;
+  const int64_t row_elems = (int64_t)kVpl * 32 * kVec;
+  // pair offset of this lane's vectors inside the head (same for all kVpl)
+  const int pair0 = (lane % vecs_per_head) * kPairs;
+  for (int64_t r0 = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r0 < total; r0 += 2 * (int64_t)warps) {
+    uint4 val[2][kVpl];
+    int tab[2];
+    int64_t base[2];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      int64_t g = base + (int64_t)u * stride;
-      live[u] = g < total_vecs;
-      tab[u] = -1;
-      off[u] = 0;
-      if (live[u]) {
-        int64_t row_all = g / vecs_per_row;  // (layer, row)
-        int vin = (int)(g - row_all * vecs_per_row);
-        int64_t layer = row_all / n_rows;
-        int64_t row = row_all - layer * n_rows;
-        int t = row_table[row];
-        off[u] = layer * layer_stride + row * (int64_t)vecs_per_row * kVec + (int64_t)vin * kVec;
-        if (t >= 0 || !in_place) val[u] = *reinterpret_cast<const V*>(src + off[u]);
-        // table offset of this vector's first pair
-        tab[u] = t >= 0 ? (t * half + (vin % vecs_per_head) * kPairs) : -1;
-      }
-    }
+    for (int q = 0; q < 2; ++q) {
+      const int64_t r = r0 + (int64_t)q * warps;
+      tab[q] = -2;
+      if (r < total) {
+        const int layer = (int)(r / n_rows);
+        const int row = (int)(r - (int64_t)layer * n_rows);
+        tab[q] = row_table[row];
+        base[q] = layer * layer_stride + row * row_elems;
+        if (tab[q] >= 0 || !in_place) {
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      if (!live[u]) continue;
-      if (tab[u] >= 0) {
-        T* e = reinterpret_cast<T*>(&val[u]);
-#pragma unroll
-        for (int p = 0; p < kPairs; ++p) {
-          float2 c = __ldg(cs + tab[u] + p);
-          float x0 = to_f32(e[2 * p]), x1 = to_f32(e[2 * p + 1]);
-          e[2 * p] = from_f32<T>(x0 * c.x - x1 * c.y);
-          e[2 * p + 1] = from_f32<T>(x0 * c.y + x1 * c.x);
+          for (int u = 0; u < kVpl; ++u)
+            val[q][u] = *reinterpret_cast<const uint4*>(src + base[q] + (int64_t)(lane + 32 * u) * kVec);
         }
-        *reinterpret_cast<V*>(dst + off[u]) = val[u];
-      } else if (!in_place) {
-        *reinterpret_cast<V*>(dst + off[u]) = val[u];
       }
     }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (tab[q] == -2 || (tab[q] < 0 && in_place)) continue;
+      if (tab[q] >= 0) {
+        float2 c[kPairs];
+#pragma unroll
+        for (int p = 0; p < kPairs; ++p) c[p] = __ldg(cs + (int64_t)tab[q] * half + pair0 + p);
+#pragma unroll
+        for (int u = 0; u < kVpl; ++u) {
+          T* e = reinterpret_cast<T*>(&val[q][u]);
+#pragma unroll
+          for (int p = 0; p < kPairs; ++p) {
+            float x0 = to_f32(e[2 * p]), x1 = to_f32(e[2 * p + 1]);
+            e[2 * p] = from_f32<T>(x0 * c[p].x - x1 * c[p].y);
+            e[2 * p + 1] = from_f32<T>(x0 * c[p].y + x1 * c[p].x);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kVpl; ++u)
+        *reinterpret_cast<uint4*>(dst + base[q] + (int64_t)(lane + 32 * u) * kVec) = val[q][u];
+    }
+  }
+}
+
+// Generic fallback: one thread per 16-byte vector (rows not a multiple of
+// 32 vectors, e.g. the tiny parity configs).
+template <typename T>
+__global__ void rotate_rows_generic_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t layer_stride,
+                                           int64_t n_rows, int vecs_per_row, int vecs_per_head, int64_t total_vecs,
+                                           const int32_t* __restrict__ row_table, const float2* __restrict__ cs,
+                                           int half, bool in_place) {
+  constexpr int kVec = 16 / sizeof(T);
+  constexpr int kPairs = kVec / 2;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total_vecs;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row_all = g / vecs_per_row;
+    const int vin = (int)(g - row_all * vecs_per_row);
+    const int64_t layer = row_all / n_rows;
+    const int64_t row = row_all - layer * n_rows;
+    const int t = row_table[row];
+    if (t < 0 && in_place) continue;
+    const int64_t off = layer * layer_stride + row * (int64_t)vecs_per_row * kVec + (int64_t)vin * kVec;
+    uint4 val = *reinterpret_cast<const uint4*>(src + off);
+    if (t >= 0) {
+      T* e = reinterpret_cast<T*>(&val);
+      const int p0 = t * half + (vin % vecs_per_head) * kPairs;
+#pragma unroll
+      for (int p = 0; p < kPairs; ++p) {
+        float2 c = __ldg(cs + p0 + p);
+        float x0 = to_f32(e[2 * p]), x1 = to_f32(e[2 * p + 1]);
+        e[2 * p] = from_f32<T>(x0 * c.x - x1 * c.y);
+        e[2 * p + 1] = from_f32<T>(x0 * c.y + x1 * c.x);
+      }
+    }
+    *reinterpret_cast<uint4*>(dst + off) = val;
   }
 }
 
@@ -161,6 +202,35 @@ __global__ void qkv_rope_scatter_kernel(const TIn* __restrict__ qkv, int n_parts
   d[1] = from_f32<TOut>(x1);
 }
 
+__device__ __forceinline__ void load8_add(const float* p, float* x) {
+  float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+  x[0] += a.x; x[1] += a.y; x[2] += a.z; x[3] += a.w; x[4] += b.x; x[5] += b.y; x[6] += b.z; x[7] += b.w;
+}
+__device__ __forceinline__ void load8_add(const __nv_bfloat16* p, float* x) {
+  uint4 v = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    float2 f = __bfloat1622float2(h[k]);
+    x[2 * k] += f.x;
+    x[2 * k + 1] += f.y;
+  }
+}
+__device__ __forceinline__ void store8(float* d, const float* x) {
+  *reinterpret_cast<float4*>(d) = make_float4(x[0], x[1], x[2], x[3]);
+  *reinterpret_cast<float4*>(d + 4) = make_float4(x[4], x[5], x[6], x[7]);
+}
+__device__ __forceinline__ void store8(__nv_bfloat16* d, const float* x) {
+  uint4 v;
+  uint32_t* o = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    __nv_bfloat162 y = __floats2bfloat162_rn(x[2 * k], x[2 * k + 1]);
+    o[k] = *reinterpret_cast<uint32_t*>(&y);
+  }
+  *reinterpret_cast<uint4*>(d) = v;
+}
+
 // Vectorised variant (Dh % 8 == 0): one thread = 8 consecutive elements
 // (4 pairs) of one head row.
 template <typename TIn, typename TOut>
@@ -180,10 +250,7 @@ __global__ void qkv_rope_scatter_vec_kernel(const TIn* __restrict__ qkv, int n_p
 #pragma unroll
     for (int u = 0; u < 8; ++u) x[u] = 0.f;
     const TIn* src = qkv + (int64_t)r * (H + 2 * Hkv) * Dh + c8;
-    for (int p = 0; p < n_parts; ++p) {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) x[u] += to_f32(src[p * part_stride + u]);
-    }
+    for (int p = 0; p < n_parts; ++p) load8_add(src + p * part_stride, x);
     if (head < H + Hkv) {
       const float2* c = cs + (int64_t)r * half + e0 / 2;
 #pragma unroll
@@ -200,8 +267,7 @@ __global__ void qkv_rope_scatter_vec_kernel(const TIn* __restrict__ qkv, int n_p
     if (head < H) d = q_out + ((int64_t)r * H + head) * Dh + e0;
     else if (head < H + Hkv) d = k_dst + (drow * Hkv + (head - H)) * Dh + e0;
     else d = v_dst + (drow * Hkv + (head - H - Hkv)) * Dh + e0;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) d[u] = from_f32<TOut>(x[u]);
+    store8(d, x);
   }
 }
 
@@ -231,29 +297,55 @@ extern "C" int ifkv_rotate_rows(int dtype, const void* src, void* dst, int64_t l
   IFKV_CHECK_ARG(d_head % vec == 0, "rotate_rows: d_head %d must be a multiple of %d", d_head, vec);
   IFKV_CHECK_ARG(((uintptr_t)src % 16 == 0) && ((uintptr_t)dst % 16 == 0) && layer_stride % vec == 0,
                  "rotate_rows: slab must be 16-byte aligned");
-  int vecs_per_head = d_head / vec;
-  int vecs_per_row = heads * vecs_per_head;
-  int64_t total = (int64_t)n_layers * n_rows * vecs_per_row;
+  const int vecs_per_head = d_head / vec;
+  const int vecs_per_row = heads * vecs_per_head;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  constexpr int kUnroll = 4;
-  int64_t want = (total + 256 * kUnroll - 1) / (256 * kUnroll);
-  int64_t cap = (int64_t)sms * 8;  // 8 x 256-thread CTAs resident per SM
-  unsigned grid = (unsigned)(want < cap ? want : cap);
-  if (grid == 0) grid = 1;
-  bool in_place = src == dst;
+  const bool in_place = src == dst;
   auto tab = reinterpret_cast<const float2*>(cs);
+  cudaStream_t st = as_stream(stream);
+  const int64_t rows = (int64_t)n_layers * n_rows;
+  const bool warp_rows = vecs_per_row % 32 == 0 && 32 % vecs_per_head == 0 && vecs_per_row / 32 <= 8;
+  if (warp_rows) {
+    const int64_t want = (rows + 15) / 16;  // 8 warps x 2 rows per CTA iteration
+    const unsigned grid = (unsigned)(want < (int64_t)sms * 8 ? (want > 0 ? want : 1) : (int64_t)sms * 8);
+    const int vpl = vecs_per_row / 32;
+#define IFKV_ROT(T, V)                                                                                     \
+  rotate_rows_kernel<T, V><<<grid, 256, 0, st>>>((const T*)src, (T*)dst, layer_stride, n_rows, n_layers, \
+                                                  vecs_per_head, row_table, tab, d_head / 2, in_place)
+    if (dtype == IFKV_BF16) {
+      if (vpl == 4) IFKV_ROT(__nv_bfloat16, 4);
+      else if (vpl == 2) IFKV_ROT(__nv_bfloat16, 2);
+      else if (vpl == 1) IFKV_ROT(__nv_bfloat16, 1);
+      else if (vpl == 8) IFKV_ROT(__nv_bfloat16, 8);
+      else goto generic;
+    } else {
+      if (vpl == 8) IFKV_ROT(float, 8);
+      else if (vpl == 4) IFKV_ROT(float, 4);
+      else if (vpl == 2) IFKV_ROT(float, 2);
+      else if (vpl == 1) IFKV_ROT(float, 1);
+      else goto generic;
+    }
+#undef IFKV_ROT
+    IFKV_LAUNCH_CHECK("rotate_rows");
+    return IFKV_OK;
+  }
+generic : {
+  const int64_t total = rows * vecs_per_row;
+  const int64_t want = (total + 255) / 256;
+  const unsigned grid = (unsigned)(want < (int64_t)sms * 8 ? want : (int64_t)sms * 8);
   if (dtype == IFKV_BF16)
-    rotate_rows_kernel<__nv_bfloat16, kUnroll><<<grid, 256, 0, as_stream(stream)>>>(
-        (const __nv_bfloat16*)src, (__nv_bfloat16*)dst, layer_stride, n_rows, vecs_per_row, vecs_per_head, total,
-        row_table, tab, d_head / 2, in_place);
+    rotate_rows_generic_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)src, (__nv_bfloat16*)dst,
+                                                                    layer_stride, n_rows, vecs_per_row, vecs_per_head,
+                                                                    total, row_table, tab, d_head / 2, in_place);
   else
-    rotate_rows_kernel<float, kUnroll><<<grid, 256, 0, as_stream(stream)>>>(
-        (const float*)src, (float*)dst, layer_stride, n_rows, vecs_per_row, vecs_per_head, total, row_table, tab,
-        d_head / 2, in_place);
+    rotate_rows_generic_kernel<float><<<grid, 256, 0, st>>>((const float*)src, (float*)dst, layer_stride, n_rows,
+                                                            vecs_per_row, vecs_per_head, total, row_table, tab,
+                                                            d_head / 2, in_place);
   IFKV_LAUNCH_CHECK("rotate_rows");
   return IFKV_OK;
+}
 }
 
 extern "C" int ifkv_rotate_queries(const float* q, int G, int M, int H, int Dh, const int32_t* qset_group,

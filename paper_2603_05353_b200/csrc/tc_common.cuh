@@ -164,6 +164,18 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 2^x on the FMA pipe (x <= 0): round-to-nearest split x = n + f, f in
+// [-1/2, 1/2], 2^f by a degree-3 minimax polynomial (max rel. error 2.9e-4,
+// below bf16's half ulp), n folded into the exponent with one IMAD.  Used for
+// a fraction of the softmax exponentials so the MUFU pipe is not the limit.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: low mantissa bits = round(x)
+  const float f = x - (t - 12582912.f);
+  const float p = fmaf(fmaf(fmaf(0.05295114f, f, 0.24165066f), f, 0.69353656f), f, 1.f);
+  return __int_as_float(__float_as_int(t) * 8388608 + __float_as_int(p));
+}
+
 __device__ __forceinline__ float max3(float a, float b, float c) {
   float d;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
