@@ -177,12 +177,20 @@ int ifkv_recompute_attn(int dtype, const void* q, const void* k_layer, const voi
                         const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows, float scale, void* out,
                         void* stream);
 /* The two implementations behind it (selected automatically): the tcgen05 /
- * TMEM / TMA kernel for bf16, Dh = 128, H/Hkv in {1,2,4,8}; and the generic
+ * TMEM / TMA kernel for bf16, Dh = 128, H/Hkv <= 16; and the generic
  * SIMT fp32-softmax kernel (fp32 mode, other head sizes). */
 int ifkv_recompute_attn_tc_supported(int dtype, int H, int Hkv, int Dh);
 int ifkv_recompute_attn_simt(int dtype, const void* q, const void* k_layer, const void* v_layer,
                              const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows, float scale,
                              void* out, void* stream);
+/* Chunk-sharded recompute: the same attention over this rank's
+ * local keys only, returning the partial softmax state -- out = normalised
+ * local context (0 when no key is visible), ml_out [S][H][2] = (max, sum exp)
+ * -- for the cross-rank merge.  horizon[i] may be -1 (no local key <= the
+ * query's global index). */
+int ifkv_recompute_attn_partial(int dtype, const void* q, const void* k_layer, const void* v_layer,
+                                const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows, float scale,
+                                void* out, float* ml_out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -256,15 +256,19 @@ def decode_view(cache: AssembledCache, rope_base: float):
     return out, cache.values
 
 
-def to_decode_layout(cache: AssembledCache, rope_base: float) -> AssembledCache:
+def to_decode_layout(cache: AssembledCache, rope_base: float, targets: Optional[np.ndarray] = None) -> AssembledCache:
     """Kernel 1 in place: rotate every context row to position = its index
-    (the layout recompute and decoding run under); updates row_positions."""
-    delta = decode_targets(cache) - cache.row_positions
+    (the layout recompute and decoding run under) -- or, for a chunk shard,
+    to its global index ``targets`` -- and update row_positions."""
+    n = cache.context_length
+    target = decode_targets(cache) if targets is None else np.concatenate(
+        [np.asarray(targets, np.int64), cache.row_positions[n:]])
+    delta = target - cache.row_positions
     if np.any(delta):
         tab, cs = _delta_table(delta, cache.keys.shape[3], rope_base, cache.keys.device)
         with E._Bracket("rotate_rows", int(np.count_nonzero(delta))):
             E.rotate_rows(cache.keys, cache.keys, tab, cs)
-        cache.row_positions[:] = decode_targets(cache)
+        cache.row_positions[:] = target
     return cache
 
 

@@ -147,7 +147,7 @@ __global__ void prompt_attn_merge_kernel(const float* __restrict__ part_ml, cons
     l += part_ml[2 * row + 1] * a;
     if (d < Dh) o += part_o[row * Dh + d] * a;
   }
-  if (d < Dh) ctx[(((int64_t)g * M + m) * H + h) * Dh + d] = o / l;
+  if (d < Dh) ctx[(((int64_t)g * M + m) * H + h) * Dh + d] = l > 0.f ? o / l : 0.f;  // no item: empty shard
   if (d == 0) {
     ml[2 * (((int64_t)g * H + h) * M + m)] = mx;
     ml[2 * (((int64_t)g * H + h) * M + m) + 1] = l;

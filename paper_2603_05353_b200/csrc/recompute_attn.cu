@@ -14,7 +14,8 @@ template <typename T>
 __global__ void __launch_bounds__(128) recompute_attn_simt_kernel(const T* __restrict__ q, const T* __restrict__ k,
                                                                   const T* __restrict__ v,
                                                                   const int64_t* __restrict__ horizon, int S, int H,
-                                                                  int Hkv, int Dh, float scale, T* __restrict__ out) {
+                                                                  int Hkv, int Dh, float scale, T* __restrict__ out,
+                                                                  float* __restrict__ ml_out) {
   extern __shared__ float smem[];
   float* Ks = smem;                          // [32][Dh+1]
   float* Vs = Ks + kRaKeys * (Dh + 1);       // [32][Dh]
@@ -39,7 +40,7 @@ __global__ void __launch_bounds__(128) recompute_attn_simt_kernel(const T* __res
 #pragma unroll
     for (int u = 0; u < 8; ++u) o[r][u] = 0.f;
   }
-  const int64_t kmax = horizon[t0 + nt - 1];
+  const int64_t kmax = horizon[t0 + nt - 1];  // -1 in partial mode: no local key visible
   for (int64_t k0 = 0; k0 <= kmax; k0 += kRaKeys) {
     __syncthreads();
     const int nk = (int)(kmax + 1 - k0 < kRaKeys ? kmax + 1 - k0 : kRaKeys);
@@ -84,10 +85,16 @@ __global__ void __launch_bounds__(128) recompute_attn_simt_kernel(const T* __res
   for (int r = 0; r < 4; ++r) {
     int row = warp * 4 + r;
     if (row >= nt) continue;
+    const int64_t orow = (int64_t)(t0 + row) * H + h;
+    const float inv = l[r] > 0.f ? 1.f / l[r] : 0.f;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       int d = lane + 32 * u;
-      if (d < Dh) out[((int64_t)(t0 + row) * H + h) * Dh + d] = from_f32<T>(o[r][u] / l[r]);
+      if (d < Dh) out[orow * Dh + d] = from_f32<T>(o[r][u] * inv);
+    }
+    if (ml_out && lane == 0) {
+      ml_out[2 * orow] = m[r];
+      ml_out[2 * orow + 1] = l[r];
     }
   }
 }
@@ -97,11 +104,12 @@ __global__ void __launch_bounds__(128) recompute_attn_simt_kernel(const T* __res
 using namespace ifkv;
 
 extern "C" int ifkv_recompute_attn_tc(const void* q, const void* k_layer, const void* v_layer, const int64_t* horizon,
-                                      int S, int H, int Hkv, int Dh, int n_rows, float scale, void* out, void* stream);
+                                      int S, int H, int Hkv, int Dh, int n_rows, float scale, void* out, float* ml_out,
+                                      void* stream);
 
-extern "C" int ifkv_recompute_attn_simt(int dtype, const void* q, const void* k_layer, const void* v_layer,
-                                        const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows, float scale,
-                                        void* out, void* stream) {
+static int recompute_attn_simt_impl(int dtype, const void* q, const void* k_layer, const void* v_layer,
+                                    const int64_t* horizon, int S, int H, int Hkv, int Dh, float scale, void* out,
+                                    float* ml_out, void* stream) {
   IFKV_CHECK_ARG(dtype == IFKV_F32 || dtype == IFKV_BF16, "recompute_attn: bad dtype");
   IFKV_CHECK_ARG(Dh % 2 == 0 && Dh <= 256 && Hkv > 0 && H % Hkv == 0, "recompute_attn: bad shape");
   if (S <= 0) return IFKV_OK;
@@ -112,21 +120,37 @@ extern "C" int ifkv_recompute_attn_simt(int dtype, const void* q, const void* k_
     IFKV_CUDA_CALL(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "recompute_attn");
     kern<<<grid, 128, sm, as_stream(stream)>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k_layer,
                                                (const __nv_bfloat16*)v_layer, horizon, S, H, Hkv, Dh, scale,
-                                               (__nv_bfloat16*)out);
+                                               (__nv_bfloat16*)out, ml_out);
   } else {
     auto kern = recompute_attn_simt_kernel<float>;
     IFKV_CUDA_CALL(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "recompute_attn");
     kern<<<grid, 128, sm, as_stream(stream)>>>((const float*)q, (const float*)k_layer, (const float*)v_layer, horizon,
-                                               S, H, Hkv, Dh, scale, (float*)out);
+                                               S, H, Hkv, Dh, scale, (float*)out, ml_out);
   }
   IFKV_LAUNCH_CHECK("recompute_attn_simt");
   return IFKV_OK;
+}
+
+extern "C" int ifkv_recompute_attn_simt(int dtype, const void* q, const void* k_layer, const void* v_layer,
+                                        const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows, float scale,
+                                        void* out, void* stream) {
+  return recompute_attn_simt_impl(dtype, q, k_layer, v_layer, horizon, S, H, Hkv, Dh, scale, out, nullptr, stream);
 }
 
 extern "C" int ifkv_recompute_attn(int dtype, const void* q, const void* k_layer, const void* v_layer,
                                    const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows, float scale,
                                    void* out, void* stream) {
   if (ifkv_recompute_attn_tc_supported(dtype, H, Hkv, Dh))
-    return ifkv_recompute_attn_tc(q, k_layer, v_layer, horizon, S, H, Hkv, Dh, n_rows, scale, out, stream);
-  return ifkv_recompute_attn_simt(dtype, q, k_layer, v_layer, horizon, S, H, Hkv, Dh, n_rows, scale, out, stream);
+    return ifkv_recompute_attn_tc(q, k_layer, v_layer, horizon, S, H, Hkv, Dh, n_rows, scale, out, nullptr, stream);
+  return recompute_attn_simt_impl(dtype, q, k_layer, v_layer, horizon, S, H, Hkv, Dh, scale, out, nullptr, stream);
+}
+
+extern "C" int ifkv_recompute_attn_partial(int dtype, const void* q, const void* k_layer, const void* v_layer,
+                                           const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows,
+                                           float scale, void* out, float* ml_out, void* stream) {
+  IFKV_CHECK_ARG(ml_out != nullptr, "recompute_attn_partial: ml_out required");
+  if (n_rows <= 0) return IFKV_ERR_ARG;
+  if (ifkv_recompute_attn_tc_supported(dtype, H, Hkv, Dh))
+    return ifkv_recompute_attn_tc(q, k_layer, v_layer, horizon, S, H, Hkv, Dh, n_rows, scale, out, ml_out, stream);
+  return recompute_attn_simt_impl(dtype, q, k_layer, v_layer, horizon, S, H, Hkv, Dh, scale, out, ml_out, stream);
 }

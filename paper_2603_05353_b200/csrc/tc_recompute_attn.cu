@@ -1,6 +1,6 @@
 // Selective-recompute attention on the 5th-gen tensor cores (tcgen05 + TMEM
 // + TMA): bf16 Q/K/V, fp32 softmax, bf16 out, Dh = 128, GQA groups of
-// G = H/Hkv in {1, 2, 4, 8} query heads per kv head.
+// G = H/Hkv <= 16 query heads per kv head (floor(128/G) tokens per tile).
 //
 // Reference: recompute.py:92-114 -- selected queries attend every context
 // key up to their own global index (masked_attention model.py:297-315).
@@ -52,18 +52,18 @@ struct Smem {
 __device__ __forceinline__ int tile_blocks(const int64_t* horizon, int t0, int tok, int S) {
   if (t0 >= S) return 0;
   const int last = min(t0 + tok, S) - 1;
-  return (int)((horizon[last] + kKeys) / kKeys);
+  return horizon[last] < 0 ? 0 : (int)((horizon[last] + kKeys) / kKeys);
 }
 
 // Softmax + epilogue of one tile; `x` = 0 (A) or 1 (B).
 __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int nblk, int t0, int S, int H, int G,
                                              int g, const int64_t* __restrict__ horizon, float scale_log2,
-                                             __nv_bfloat16* __restrict__ out) {
+                                             __nv_bfloat16* __restrict__ out, float* __restrict__ ml_out) {
   const int w = (threadIdx.x >> 5) & 3;  // lane quarter of TMEM this warp may access
   const int lane = threadIdx.x & 31;
   const int row = w * 32 + lane;
   const int tok = t0 + row / G;
-  const bool valid = tok < S;
+  const bool valid = row < (kRows / G) * G && tok < S;  // G not dividing 128 leaves pad rows
   const int hz = valid ? (int)horizon[tok] : 0;
   const uint32_t lane_off = (uint32_t)(w * 32) << 16;
   const uint32_t t_s = tmem + 256 * x + lane_off;
@@ -142,16 +142,28 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
     tc::tc_fence_before();
     tc::mbar_arrive(&sm.p_full[x]);
   }
-  // epilogue
-  tc::mbar_wait(&sm.o_final[x], 0);
-  tc::tc_fence_after();
-  const float inv = 1.f / l;
-  __nv_bfloat16* dst = out + ((int64_t)tok * H + g * G + row % G) * kDh;
+  // epilogue (a row that saw no key -- horizon -1 in partial mode -- writes 0)
+  if (nblk > 0) {
+    tc::mbar_wait(&sm.o_final[x], 0);
+    tc::tc_fence_after();
+  }
+  const float inv = l > 0.f ? 1.f / l : 0.f;
+  const int64_t orow = (int64_t)tok * H + g * G + row % G;
+  __nv_bfloat16* dst = out + orow * kDh;
+  if (ml_out && valid) {
+    ml_out[2 * orow] = m_used;
+    ml_out[2 * orow + 1] = l;
+  }
 #pragma unroll
   for (int c = 0; c < kDh / 32; ++c) {
     float o[32];
-    tc::tmem_ld32(t_o + c * 32, o);
-    tc::tmem_ld_wait();
+    if (nblk > 0) {
+      tc::tmem_ld32(t_o + c * 32, o);
+      tc::tmem_ld_wait();
+    } else {
+#pragma unroll
+      for (int u = 0; u < 32; ++u) o[u] = 0.f;
+    }
     if (valid) {
 #pragma unroll
       for (int u = 0; u < 32; u += 8) {
@@ -169,7 +181,8 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
 __global__ void __launch_bounds__(384, 1)
     recompute_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                              const __grid_constant__ CUtensorMap tm_v, const int64_t* __restrict__ horizon, int S,
-                             int H, int Hkv, float scale_log2, __nv_bfloat16* __restrict__ out) {
+                             int H, int Hkv, float scale_log2, __nv_bfloat16* __restrict__ out,
+                             float* __restrict__ ml_out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -207,7 +220,7 @@ __global__ void __launch_bounds__(384, 1)
       tc::tma_prefetch(&tm_q);
       tc::tma_prefetch(&tm_k);
       tc::tma_prefetch(&tm_v);
-      tc::mbar_arrive_expect_tx(&sm.q_full, (nB > 0 ? 2 : 1) * kTile);
+      tc::mbar_arrive_expect_tx(&sm.q_full, (nB > 0 ? 2 : 1) * 2 * 128 * (tok * G));  // box = tok x G rows
       tc::tma_load_3d(sm.q[0], &tm_q, &sm.q_full, 0, g * G, tA);
       tc::tma_load_3d(sm.q[0] + kPanel, &tm_q, &sm.q_full, 64, g * G, tA);
       if (nB > 0) {
@@ -288,7 +301,8 @@ __global__ void __launch_bounds__(384, 1)
     tc::reg_alloc<208>();
     const int x = (warp - 4) >> 2;  // 0: tile A (warps 4-7), 1: tile B (warps 8-11)
     const int nx = x == 0 ? nA : nB;
-    if (nx > 0) softmax_tile(sm, tmem, x, nx, x == 0 ? tA : tB, S, H, G, g, horizon, scale_log2, out);
+    const int tx = x == 0 ? tA : tB;
+    if (tx < S) softmax_tile(sm, tmem, x, nx, tx, S, H, G, g, horizon, scale_log2, out, ml_out);
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -302,12 +316,11 @@ using namespace ifkv;
 
 extern "C" int ifkv_recompute_attn_tc_supported(int dtype, int H, int Hkv, int Dh) {
   if (dtype != IFKV_BF16 || Dh != kDh || Hkv <= 0 || H % Hkv) return 0;
-  int G = H / Hkv;
-  return (G == 1 || G == 2 || G == 4 || G == 8) ? 1 : 0;
+  return H / Hkv <= 16 ? 1 : 0;  // a tile holds floor(128 / G) tokens x G heads
 }
 
 extern "C" int ifkv_recompute_attn_tc(const void* q, const void* k_layer, const void* v_layer, const int64_t* horizon,
-                                      int S, int H, int Hkv, int Dh, int n_rows, float scale, void* out,
+                                      int S, int H, int Hkv, int Dh, int n_rows, float scale, void* out, float* ml_out,
                                       void* stream) {
   IFKV_CHECK_ARG(ifkv_recompute_attn_tc_supported(IFKV_BF16, H, Hkv, Dh), "recompute_attn_tc: unsupported shape");
   if (S <= 0) return IFKV_OK;
@@ -337,7 +350,7 @@ extern "C" int ifkv_recompute_attn_tc(const void* q, const void* k_layer, const 
   dim3 grid(Hkv, (S + tok_per_pair - 1) / tok_per_pair);
   const float scale_log2 = scale * 1.4426950408889634f;
   recompute_attn_tc_kernel<<<grid, 384, smem, as_stream(stream)>>>(tq, tk, tv, horizon, S, H, Hkv, scale_log2,
-                                                                    (__nv_bfloat16*)out);
+                                                                    (__nv_bfloat16*)out, ml_out);
   IFKV_LAUNCH_CHECK("recompute_attn_tc");
   return IFKV_OK;
 }

@@ -200,6 +200,18 @@ def topk_segments(scores, seg_begin, seg_k, agg_mode: int = N.AGG_NONE):
     return out, agg, out_begin
 
 
+def recompute_attn_partial(q, k_layer, v_layer, horizon, H, Hkv, Dh):
+    """Attention of q over this shard's keys only: (normalised ctx, ml [S,H,2])."""
+    torch = _torch()
+    S = q.shape[0]
+    out = torch.empty_like(q)
+    ml = torch.empty((S, H, 2), dtype=torch.float32, device=q.device)
+    if S:
+        N.call("ifkv_recompute_attn_partial", dt_code(q), N.ptr(q), N.ptr(k_layer), N.ptr(v_layer), N.ptr(horizon),
+               S, H, Hkv, Dh, k_layer.shape[0], 1.0 / math.sqrt(Dh), N.ptr(out), N.ptr(ml), _s())
+    return out, ml
+
+
 def recompute_attn(q, k_layer, v_layer, horizon, H, Hkv, Dh, out=None, impl: str = "auto"):
     """impl: "auto" (tcgen05 when supported, else SIMT) or "simt"."""
     torch = _torch()
@@ -310,11 +322,14 @@ def _tc_item_keys(groups, Hkv: int, G: int, M: int, sms: int = 148) -> int:
 
 
 def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], capture_layer: Optional[int] = None,
-                   want_logits: bool = False, impl: str = "auto") -> PromptOut:
+                   want_logits: bool = False, impl: str = "auto", merge_hook=None,
+                   include_prompt: bool = True) -> PromptOut:
     """Run every group's prompt forward; capture column scores at
     ``capture_layer`` (then stop) or return last-row logits.  impl "auto"
     uses the tcgen05 kernels for bf16 slabs with Dh = 128, "simt" forces the
-    generic kernels."""
+    generic kernels.  Chunk sharding: ``merge_hook(ctx, ml) -> (ctx, ml)``
+    merges this rank's attention state with the other ranks' after every
+    layer, and ``include_prompt`` adds the prompt's own keys (one rank only)."""
     torch = _torch()
     cfg = weights.config
     dev = weights.device
@@ -370,21 +385,28 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
                N.ptr(qd3), _s())
         capture = capture_layer is not None and li == capture_layer
         with _Bracket("prompt_attn", li):
-            if use_tc:
+            if use_tc and n_ctx:
                 N.call("ifkv_prompt_attn_partial_tc", N.ptr(qd3), n_qsets, N.ptr(slab_k[li]), N.ptr(slab_v[li]),
                        n_rows, items_p, n_ctx, item_keys, H, Hkv, M, scale, N.ptr(part_ml), N.ptr(part_o), _s())
+            elif n_ctx:
+                N.call("ifkv_prompt_attn_partial", kv_dt, N.ptr(qd), N.ptr(slab_k[li]), N.ptr(slab_v[li]), N.ptr(kp),
+                       N.ptr(vp), items_p, n_ctx, H, Hkv, M, Dh, scale, N.ptr(part_ml), N.ptr(part_o), _s())
+            if include_prompt:
                 N.call("ifkv_prompt_attn_partial", kv_dt, N.ptr(qd), N.ptr(slab_k[li]), N.ptr(slab_v[li]), N.ptr(kp),
                        N.ptr(vp), prompt_items_p, n_items - n_ctx, H, Hkv, M, Dh, scale,
                        part_ml.data_ptr() + n_ctx * stride_ml, part_o.data_ptr() + n_ctx * stride_o, _s())
-            else:
-                N.call("ifkv_prompt_attn_partial", kv_dt, N.ptr(qd), N.ptr(slab_k[li]), N.ptr(slab_v[li]), N.ptr(kp),
-                       N.ptr(vp), items_p, n_items, H, Hkv, M, Dh, scale, N.ptr(part_ml), N.ptr(part_o), _s())
-            N.call("ifkv_prompt_attn_merge", N.ptr(part_ml), N.ptr(part_o), ib_p, n_ctx, G, H, M, Dh, N.ptr(ctx),
-                   N.ptr(ml), _s())
+            N.call("ifkv_prompt_attn_merge", N.ptr(part_ml), N.ptr(part_o), ib_p, n_ctx if include_prompt else -1, G,
+                   H, M, Dh, N.ptr(ctx), N.ptr(ml), _s())
+            if merge_hook is not None:
+                ctx_m, ml_m = merge_hook(ctx, ml)
+                ctx.copy_(ctx_m)
+                ml.copy_(ml_m)
         if capture:
             scores = torch.zeros(n_rows, dtype=torch.float32, device=dev)
             with _Bracket("score_columns", li):
-                if use_tc:
+                if not n_ctx:
+                    pass
+                elif use_tc:
                     hpt = min(128 // M, H // Hkv)
                     n_chunks = Hkv * (-(-(H // Hkv) // hpt))
                     ws = torch.empty((n_ctx, n_chunks, item_keys), dtype=torch.float32, device=dev)
@@ -414,7 +436,8 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
 # ---------------------------------------------------------------------------
 
 
-def layer_stack(weights, token_ids, positions, k_slab, v_slab, dst_rows, horizon, want_hidden: bool = False):
+def layer_stack(weights, token_ids, positions, k_slab, v_slab, dst_rows, horizon, want_hidden: bool = False,
+                attn_fn=None):
     """Advance S tokens (device int64 ids/positions) through every layer.
 
     Layer l: x = rms_norm(h); q,k,v = x W; rope at ``positions``; k,v written
@@ -427,8 +450,8 @@ def layer_stack(weights, token_ids, positions, k_slab, v_slab, dst_rows, horizon
     dev = weights.device
     H, Hkv, Dh, d = cfg.n_heads, cfg.kv_heads, cfg.d_head, cfg.d_model
     S = int(token_ids.numel())
-    if S == 0:
-        return None
+    if S == 0 and attn_fn is None:
+        return None  # (sharded ranks keep looping: every layer has collectives)
     bf16 = weights.precision == "bf16"
     act_mode = N.OUT_BF16 if bf16 else N.OUT_F32
     cs = rope_table(positions, Dh, cfg.rope_base, dev)
@@ -443,8 +466,11 @@ def layer_stack(weights, token_ids, positions, k_slab, v_slab, dst_rows, horizon
         qkv_rope_scatter(qkv, 1, H, Hkv, Dh, cs, None if final else qbuf, k_slab[li], v_slab[li], dst_rows)
         if final:
             return None
-        with _Bracket("recompute_attn", li):
-            recompute_attn(qbuf, k_slab[li], v_slab[li], horizon, H, Hkv, Dh, out=attn_out)
+        if attn_fn is not None:  # chunk-sharded: attention over every rank's keys
+            attn_out = attn_fn(li, qbuf, k_slab[li], v_slab[li])
+        else:
+            with _Bracket("recompute_attn", li):
+                recompute_attn(qbuf, k_slab[li], v_slab[li], horizon, H, Hkv, Dh, out=attn_out)
         o = torch.mm(attn_out.view(S, d), lw.wo, out_dtype=torch.float32) if bf16 else torch.mm(attn_out.view(S, d),
                                                                                                  lw.wo)
         x2 = add_rmsnorm(h, o, 1, lw.mlp_norm, act_mode)

@@ -1,0 +1,335 @@
+"""Chunk-sharded query-time context assembly across the GPUs of one box
+(the reference has no distributed path -- its cost model
+`costmodel.py:127-177` describes the "communicate only the selected tokens"
+scheme this implements).
+
+Layout: chunk c lives on rank ``zigzag_owners(K, R)[c]`` (zig-zag over 2R
+slots so every rank holds early and late chunks and the causal work is
+balanced).  Each rank keeps only its chunks' KV (its own assembled slab,
+local rows in ascending global order) and a replica of the weights.
+
+Scoring (selection.py:127-183): every rank runs the prompt forward against
+its own chunks; after every layer the per-rank softmax states (normalised
+context, max, sum) are all-gathered and merged in rank order (identical on
+every rank, deterministic); the prompt's own keys are counted once (rank 0).
+At the capture layer each rank scores its own rows with the merged (max, sum)
+and takes a local top-k; the (score, global index) candidates are
+all-gathered and merged with the reference's tie rule -- exact, because the
+global top-k is contained in the union of the local top-k's.
+
+Recompute (recompute.py:67-122): every rank advances the selected tokens it
+owns through the layer stack (weights replicated, owner-computes) and
+scatters their K/V into its slab; per layer the selected queries are
+all-gathered, every rank computes partial causal attention of all of them
+against its local keys (``ifkv_recompute_attn_partial``), and the partials
+are sent back to the owners (all-to-all) and merged in rank order.  Traffic
+per layer is O(k), not ring attention's O(N).
+
+``TorchComm`` runs the collectives over torch.distributed (NCCL on GPUs, gloo
+on CPU tensors); ``ThreadComm`` runs R ranks as threads of one process on one
+device so the sharded data path is exercised on a single GPU.
+"""
+
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass
+from typing import Callable, List, Optional, Sequence
+
+import numpy as np
+
+from . import engine as E
+from .cache import AssembledCache, Provenance, to_decode_layout
+from .errors import ConfigurationError
+from .selection import SelectionConfig, SelectionResult, default_norm_layer
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+# ---------------------------------------------------------------------------
+# communicators
+# ---------------------------------------------------------------------------
+
+
+class Comm:
+    """Single-rank communicator (collectives are identities)."""
+
+    world = 1
+    rank = 0
+
+    def all_gather(self, t) -> list:
+        return [t]
+
+    def all_to_all(self, parts: list) -> list:
+        return list(parts)
+
+    def all_gather_var(self, t) -> list:
+        """all_gather for tensors whose first dimension differs per rank."""
+        return self.all_gather(t)
+
+
+class TorchComm(Comm):
+    """torch.distributed collectives (NCCL for CUDA tensors, gloo for CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist, self.group = dist, group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def all_gather(self, t):
+        t = t.contiguous()
+        out = [t.new_empty(t.shape) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return out
+
+    def _sizes(self, n: int, device):
+        torch = _torch()
+        s = torch.tensor([n], dtype=torch.int64, device=device)
+        return [int(x.item()) for x in self.all_gather(s)]
+
+    def all_gather_var(self, t):
+        t = t.contiguous()
+        sizes = self._sizes(t.shape[0], t.device)
+        cap = max(sizes) if sizes else 0
+        pad = t.new_zeros((cap,) + tuple(t.shape[1:]))
+        pad[: t.shape[0]] = t
+        return [x[:n] for x, n in zip(self.all_gather(pad), sizes)]
+
+    def all_to_all(self, parts):
+        parts = [p.contiguous() for p in parts]
+        # receive sizes first (first dimension may differ)
+        torch = _torch()
+        send_n = torch.tensor([p.shape[0] for p in parts], dtype=torch.int64, device=parts[0].device)
+        recv_n = torch.empty_like(send_n)
+        self.dist.all_to_all_single(recv_n, send_n, group=self.group)
+        recv = [parts[0].new_empty((int(n),) + tuple(parts[0].shape[1:])) for n in recv_n.tolist()]
+        self.dist.all_to_all(recv, parts, group=self.group)
+        return recv
+
+
+class ThreadComm(Comm):
+    """R ranks as threads of one process sharing one device (collectives are
+    list exchanges behind a barrier).  Used to run the sharded data path,
+    kernels included, on a single GPU."""
+
+    def __init__(self, world: int, rank: int, shared: dict):
+        self.world, self.rank, self.shared = world, rank, shared
+
+    @staticmethod
+    def run(world: int, fn: Callable[["ThreadComm"], object]) -> list:
+        shared = {"slots": [None] * world, "barrier": threading.Barrier(world)}
+        results, errors = [None] * world, [None] * world
+
+        def body(r):
+            try:
+                results[r] = fn(ThreadComm(world, r, shared))
+            except BaseException as exc:  # noqa: BLE001 -- re-raised below
+                errors[r] = exc
+                shared["barrier"].abort()
+
+        threads = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        for e in errors:
+            if e is not None and not isinstance(e, threading.BrokenBarrierError):
+                raise e
+        for e in errors:
+            if e is not None:
+                raise e
+        return results
+
+    def _exchange(self, value, pick):
+        """Publish `value`, read the others' through `pick` (which copies), and
+        only then release the writers: every copy is enqueued on the shared
+        stream before any rank can enqueue a write to its published tensors."""
+        slots, bar = self.shared["slots"], self.shared["barrier"]
+        slots[self.rank] = value
+        bar.wait()
+        out = [pick(r, slots[r]) for r in range(self.world)]
+        bar.wait()
+        return out
+
+    def all_gather(self, t):
+        return self._exchange(t, lambda r, x: x if r == self.rank else x.clone())
+
+    def all_gather_var(self, t):
+        return self.all_gather(t)
+
+    def all_to_all(self, parts):
+        return self._exchange(list(parts), lambda r, x: x[self.rank].clone())
+
+
+# ---------------------------------------------------------------------------
+# layout
+# ---------------------------------------------------------------------------
+
+
+def zigzag_owners(n_chunks: int, world: int) -> np.ndarray:
+    """Chunk c -> rank: slot c mod 2R, folded (r, 2R-1-r) so each rank gets
+    one early and one late chunk per 2R chunks (balanced causal work)."""
+    slot = np.arange(n_chunks) % (2 * world)
+    return np.where(slot < world, slot, 2 * world - 1 - slot).astype(np.int64)
+
+
+@dataclass
+class Shard:
+    rank: int
+    world: int
+    chunk_ids: List[int]  # global declared-order indices of the owned chunks (ascending)
+    global_rows: np.ndarray  # global context index of every local row (ascending)
+    n_context: int
+
+
+def make_shard(chunk_lengths: Sequence[int], rank: int, world: int, owners: Optional[np.ndarray] = None) -> Shard:
+    lens = np.asarray(chunk_lengths, np.int64)
+    owners = zigzag_owners(len(lens), world) if owners is None else np.asarray(owners)
+    starts = np.concatenate([[0], np.cumsum(lens)[:-1]])
+    mine = [int(c) for c in np.flatnonzero(owners == rank)]
+    rows = [starts[c] + np.arange(lens[c]) for c in mine]
+    return Shard(rank, world, mine, np.concatenate(rows).astype(np.int64) if rows else np.zeros(0, np.int64),
+                 int(lens.sum()))
+
+
+# ---------------------------------------------------------------------------
+# merges (fixed rank order -> identical, deterministic results on every rank)
+# ---------------------------------------------------------------------------
+
+
+def merge_softmax_states(ctxs: Sequence, mls: Sequence, head_axis_ml: bool = True):
+    """Merge per-rank softmax states.  ctx_r: normalised context (any float
+    dtype), ml_r: (max, sum) in the last dim, broadcast-compatible with ctx_r
+    after unsqueezing the feature dim.  Returns (ctx fp32, ml)."""
+    torch = _torch()
+    m = torch.stack([x[..., 0] for x in mls])  # [R, ...]
+    l = torch.stack([x[..., 1] for x in mls])
+    mx = torch.max(m, dim=0).values
+    safe = torch.where(torch.isfinite(mx), mx, torch.zeros_like(mx))
+    w = torch.where(l > 0, l * torch.exp(m - safe), torch.zeros_like(l))  # [R, ...]
+    lt = w.sum(0)
+    return w, mx, lt
+
+
+def merge_prompt_states(ctxs: Sequence, mls: Sequence):
+    """ctx_r [G, M, H, Dh] fp32, ml_r [G, H, M, 2] -> merged (ctx, ml)."""
+    torch = _torch()
+    w, mx, lt = merge_softmax_states(ctxs, mls)
+    acc = torch.zeros_like(ctxs[0])
+    for r, c in enumerate(ctxs):
+        acc += c * w[r].transpose(1, 2).unsqueeze(-1)  # [G, H, M] -> [G, M, H, 1]
+    ctx = acc / torch.where(lt > 0, lt, torch.ones_like(lt)).transpose(1, 2).unsqueeze(-1)
+    return ctx, torch.stack([mx, lt], dim=-1)
+
+
+def merge_query_states(ctxs: Sequence, mls: Sequence):
+    """ctx_r [S, H, Dh], ml_r [S, H, 2] -> merged normalised ctx [S, H, Dh]
+    (fp32, or fp64 for fp64 inputs)."""
+    torch = _torch()
+    w, _, lt = merge_softmax_states(ctxs, mls)
+    dt = torch.float64 if ctxs[0].dtype == torch.float64 else torch.float32
+    acc = torch.zeros(ctxs[0].shape, dtype=dt, device=ctxs[0].device)
+    for r, c in enumerate(ctxs):
+        acc += c.to(dt) * w[r].to(dt).unsqueeze(-1)
+    return acc / torch.where(lt > 0, lt, torch.ones_like(lt)).unsqueeze(-1)
+
+
+def merge_topk(scores: Sequence, indices: Sequence, k: int):
+    """Global top-k of per-rank candidates by (score desc, global index asc),
+    returned ascending -- the reference's rule (selection.py:172-183)."""
+    torch = _torch()
+    s = torch.cat([x.float().reshape(-1) for x in scores])
+    i = torch.cat([x.reshape(-1) for x in indices]).to(torch.int64)
+    if k > s.numel():
+        raise ConfigurationError(f"k ({k}) exceeds candidate count ({s.numel()})")
+    b = s.view(torch.int32).to(torch.int64)
+    b = torch.where(s == 0, torch.zeros_like(b), b)  # -0 == +0
+    key = torch.where(b < 0, -(b & 0x7FFFFFFF) - 1, b)  # order-preserving int for float bits
+    # sort by score desc, then index asc (stable sort on index first)
+    o = torch.argsort(i, stable=True)
+    o = o[torch.argsort(key[o], descending=True, stable=True)]
+    return torch.sort(i[o[:k]]).values
+
+
+# ---------------------------------------------------------------------------
+# sharded path
+# ---------------------------------------------------------------------------
+
+
+def sharded_select(weights, shard: Shard, cache: AssembledCache, prompt_token_ids, config: SelectionConfig,
+                   comm: Comm) -> SelectionResult:
+    """Attention-norm selection (GLOBAL geometry) over chunk shards.  Returns
+    the global selected set (identical on every rank) and this rank's scores
+    for its local rows."""
+    torch = _torch()
+    cfg = weights.config
+    prompt = np.asarray(prompt_token_ids, np.int64)
+    n_local = cache.context_length
+    if n_local != shard.global_rows.size:
+        raise ConfigurationError("shard cache does not match the shard layout")
+    nl = config.norm_layer if config.norm_layer is not None else default_norm_layer(cfg.n_layers)
+    N = shard.n_context
+    prompt_pos = N + np.arange(prompt.size, dtype=np.int64)
+    group = E.PromptGroup(prompt, prompt_pos, E.segments_from_deltas(shard.global_rows - cache.row_positions[:n_local]))
+
+    def hook(ctx, ml):
+        return merge_prompt_states(comm.all_gather(ctx), comm.all_gather(ml))
+
+    out = E.prompt_forward(weights, cache.keys, cache.values, [group], capture_layer=nl, merge_hook=hook,
+                           include_prompt=shard.rank == 0)
+    scores = out.scores[:n_local]
+    k = config.resolve_budget(N)
+    kl = min(k, n_local)
+    if kl:
+        from .selection import select_topk
+
+        loc = select_topk(scores, kl)
+    else:
+        loc = torch.zeros(0, dtype=torch.int64, device=scores.device)
+    grows = torch.as_tensor(shard.global_rows, device=scores.device)
+    cand_idx = grows.index_select(0, loc)
+    cand_s = scores.index_select(0, loc)
+    sel = merge_topk(comm.all_gather_var(cand_s), comm.all_gather_var(cand_idx), k)
+    return SelectionResult(scores=scores, selected=sel, strategy="attention-norm", geometry="GLOBAL")
+
+
+def sharded_recompute(weights, shard: Shard, cache: AssembledCache, selected_global, comm: Comm) -> AssembledCache:
+    """Recompute the globally selected tokens, each on the rank owning it,
+    with attention over every rank's keys; K/V scattered into the owners'
+    slabs in place.  Every rank must call this (collectives per layer)."""
+    torch = _torch()
+    cfg = weights.config
+    dev = cache.keys.device
+    H, Hkv, Dh = cfg.n_heads, cfg.kv_heads, cfg.d_head
+    grows_np = shard.global_rows
+    grows = torch.as_tensor(grows_np, device=dev)
+    sel = torch.as_tensor(selected_global, device=dev).to(torch.int64)
+    pos = torch.searchsorted(grows, sel)
+    mine = (pos < grows.numel()) & (grows.index_select(0, pos.clamp(max=max(grows.numel() - 1, 0))) == sel) \
+        if grows.numel() else torch.zeros_like(sel, dtype=torch.bool)
+    sel_g = sel[mine]  # global indices of my selected tokens (ascending)
+    dst = pos[mine]  # their local slab rows
+    to_decode_layout(cache, cfg.rope_base, targets=grows_np)
+    ids = cache.token_ids_device().index_select(0, dst)
+
+    def attn_fn(li, q_local, k_layer, v_layer):
+        q_all = torch.cat(comm.all_gather_var(q_local))
+        hz_parts = comm.all_gather_var(sel_g)
+        sizes = [int(h.numel()) for h in hz_parts]
+        hz_local = torch.searchsorted(grows, torch.cat(hz_parts), right=True) - 1
+        ctx, ml = E.recompute_attn_partial(q_all, k_layer, v_layer, hz_local, H, Hkv, Dh)
+        back_ctx = comm.all_to_all(list(torch.split(ctx, sizes)))
+        back_ml = comm.all_to_all(list(torch.split(ml, sizes)))
+        return merge_query_states(back_ctx, back_ml).to(q_local.dtype)
+
+    E.layer_stack(weights, ids, sel_g, cache.keys, cache.values, dst, sel_g, attn_fn=attn_fn)
+    d = dst.cpu().numpy()
+    cache.row_positions[d] = sel_g.cpu().numpy()
+    cache.provenance[d] = int(Provenance.RECOMPUTED_GLOBAL)
+    return cache

@@ -136,7 +136,7 @@ def test_recompute_attention_kernel(T, cuda, dtype, hkv, dh):
     assert np.max(np.abs(got - want)) <= tol * np.max(np.abs(want))
 
 
-@pytest.mark.parametrize("G", [1, 2, 4, 8])
+@pytest.mark.parametrize("G", [1, 2, 4, 7, 8])
 def test_recompute_attention_tcgen05_vs_simt(T, cuda, G):
     """The tcgen05 kernel against the SIMT fp32-softmax kernel (and the oracle)
     on a multi-block causal span: 4096 keys, 700 selected rows."""
