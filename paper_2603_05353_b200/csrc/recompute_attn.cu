@@ -40,7 +40,8 @@ __global__ void __launch_bounds__(128) recompute_attn_simt_kernel(const T* __res
 #pragma unroll
     for (int u = 0; u < 8; ++u) o[r][u] = 0.f;
   }
-  const int64_t kmax = horizon[t0 + nt - 1];  // -1 in partial mode: no local key visible
+  int64_t kmax = -1;  // largest horizon of the tile (-1 in partial mode: no local key visible)
+  for (int r = 0; r < nt; ++r) kmax = max(kmax, horizon[t0 + r]);
   for (int64_t k0 = 0; k0 <= kmax; k0 += kRaKeys) {
     __syncthreads();
     const int nk = (int)(kmax + 1 - k0 < kRaKeys ? kmax + 1 - k0 : kRaKeys);

@@ -47,12 +47,18 @@ struct Smem {
   uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
   uint64_t s_full[2], p_full[2], o_final[2];
   uint32_t tmem_base;
+  int n_blocks[2];
 };
 
-__device__ __forceinline__ int tile_blocks(const int64_t* horizon, int t0, int tok, int S) {
-  if (t0 >= S) return 0;
-  const int last = min(t0 + tok, S) - 1;
-  return horizon[last] < 0 ? 0 : (int)((horizon[last] + kKeys) / kKeys);
+// Key blocks a tile needs: its largest horizon decides (horizons are
+// ascending on the single-GPU path, but not across the rank-ordered query
+// lists of the chunk-sharded path).  Computed by one warp, lane-strided.
+__device__ __forceinline__ int tile_blocks_warp(const int64_t* horizon, int t0, int tok, int S) {
+  int64_t mx = -1;
+  for (int t = t0 + (threadIdx.x & 31); t < min(t0 + tok, S); t += 32) mx = max(mx, horizon[t]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)mx, o));
+  return mx < 0 ? 0 : (int)((mx + kKeys) / kKeys);
 }
 
 // Softmax + epilogue of one tile; `x` = 0 (A) or 1 (B).
@@ -191,9 +197,14 @@ __global__ void __launch_bounds__(384, 1)
   const int g = blockIdx.x;
   const int pair = gridDim.y - 1 - blockIdx.y;  // heaviest (latest) tile pairs first
   const int tA = pair * 2 * tok, tB = tA + tok;
-  const int nA = tile_blocks(horizon, tA, tok, S);
-  const int nB = tile_blocks(horizon, tB, tok, S);
-  const int nblk = max(nA, nB);
+  if (warp == 3) {
+    const int a = tA < S ? tile_blocks_warp(horizon, tA, tok, S) : 0;
+    const int b = tB < S ? tile_blocks_warp(horizon, tB, tok, S) : 0;
+    if (lane == 0) {
+      sm.n_blocks[0] = a;
+      sm.n_blocks[1] = b;
+    }
+  }
 
   if (threadIdx.x == 0) {
     tc::mbar_init(&sm.q_full, 1);
@@ -213,6 +224,8 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
+  const int nA = sm.n_blocks[0], nB = sm.n_blocks[1];
+  const int nblk = max(nA, nB);
 
   if (warp < 4) {
     tc::reg_dealloc<56>();

@@ -158,3 +158,35 @@ def test_recompute_attention_tcgen05_vs_simt(T, cuda, G):
     scale = np.max(np.abs(want))
     assert np.max(np.abs(simt - want)) <= 1e-2 * scale
     assert np.max(np.abs(tc - want)) <= 1e-2 * scale
+
+
+@pytest.mark.parametrize("partial", [False, True])
+def test_recompute_attention_unsorted_and_empty_horizons(T, cuda, partial):
+    """Rank-ordered query lists (two ascending runs) and, in partial mode,
+    rows that see no key (horizon -1): the tile span is the tile's max horizon."""
+    from paper_2603_05353_b200 import engine as E
+
+    rng = np.random.default_rng(11)
+    hkv, dh, n, H = 8, 128, 3000, 32
+    a = np.sort(rng.choice(n, 250, replace=False))
+    b = np.sort(rng.choice(n, 200, replace=False))
+    hz = np.concatenate([a, b])
+    if partial:
+        hz[:7] = -1
+    q = T.as_tensor(rng.standard_normal((hz.size, H, dh)), dtype=T.float32).to(cuda, T.bfloat16)
+    k = T.as_tensor(rng.standard_normal((n, hkv, dh)), dtype=T.float32).to(cuda, T.bfloat16)
+    v = T.as_tensor(rng.standard_normal((n, hkv, dh)), dtype=T.float32).to(cuda, T.bfloat16)
+    hzt = T.as_tensor(hz, device=cuda)
+    if partial:
+        out, ml = E.recompute_attn_partial(q, k, v, hzt, H, hkv, dh)
+        ml = ml.cpu().numpy()
+        assert np.all(ml[:7, :, 1] == 0) and np.all(np.isneginf(ml[:7, :, 0]))
+        assert np.all(out[:7].float().cpu().numpy() == 0)
+        rows = slice(7, None)
+    else:
+        out = E.recompute_attn(q, k, v, hzt, H, hkv, dh)
+        rows = slice(0, None)
+    got = out.double().cpu().numpy()[rows]
+    want, _ = O.prefix_attention(q.double().cpu().numpy()[rows], k.double().cpu().numpy(), v.double().cpu().numpy(),
+                                 hz[rows])
+    assert np.max(np.abs(got - want)) <= 1e-2 * np.max(np.abs(want))
