@@ -23,6 +23,7 @@ from .cache import (
     replace_entries,
     to_decode_layout,
 )
+from .decode import first_token_logits, greedy_token
 from .errors import ChunkKVError, ConfigurationError, DataFormatError, NativeError
 from .model import (
     DeviceWeights,

@@ -169,11 +169,12 @@ __device__ __forceinline__ float ex2(float x) {
 // below bf16's half ulp), n folded into the exponent with one IMAD.  Used for
 // a fraction of the softmax exponentials so the MUFU pipe is not the limit.
 __device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -126.f);
-  const float t = x + 12582912.f;  // 1.5 * 2^23: low mantissa bits = round(x)
-  const float f = x - (t - 12582912.f);
+  const float xc = fmaxf(x, -126.f);
+  const float t = xc + 12582912.f;  // 1.5 * 2^23: low mantissa bits = round(x)
+  const float f = xc - (t - 12582912.f);
   const float p = fmaf(fmaf(fmaf(0.05295114f, f, 0.24165066f), f, 0.69353656f), f, 1.f);
-  return __int_as_float(__float_as_int(t) * 8388608 + __float_as_int(p));
+  const float r = __int_as_float(__float_as_int(t) * 8388608 + __float_as_int(p));
+  return x < -126.f ? 0.f : r;  // masked (-inf) and underflowing inputs give exactly 0, like ex2.approx.ftz
 }
 
 __device__ __forceinline__ float max3(float a, float b, float c) {

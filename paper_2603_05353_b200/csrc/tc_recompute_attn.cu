@@ -80,21 +80,20 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
     tc::tc_fence_after();
     const int j0 = j * kKeys;
     const bool masked = __any_sync(0xffffffffu, j0 + kKeys - 1 > hz);
-    float v[64];
-    // pass 1: row max over the block (two 64-column halves)
+    float v[32];
+    // pass 1: row max over the block, 32 columns at a time
     float mx = -INFINITY;
 #pragma unroll
-    for (int hf = 0; hf < 2; ++hf) {
-      tc::tmem_ld32(t_s + hf * 64, v);
-      tc::tmem_ld32(t_s + hf * 64 + 32, v + 32);
+    for (int q = 0; q < 4; ++q) {
+      tc::tmem_ld32(t_s + q * 32, v);
       tc::tmem_ld_wait();
       if (masked) {
 #pragma unroll
-        for (int c = 0; c < 64; ++c)
-          if (j0 + hf * 64 + c > hz) v[c] = -INFINITY;
+        for (int c = 0; c < 32; ++c)
+          if (j0 + q * 32 + c > hz) v[c] = -INFINITY;
       }
 #pragma unroll
-      for (int c = 0; c < 64; c += 2) mx = tc::max3(mx, v[c], v[c + 1]);
+      for (int c = 0; c < 32; c += 2) mx = tc::max3(mx, v[c], v[c + 1]);
     }
     float alpha = 1.f;
     bool need = false;
@@ -109,29 +108,28 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
       const float a = need ? alpha : 1.f;
 #pragma unroll
       for (int c = 0; c < kDh / 32; ++c) {
-        float o[32];
-        tc::tmem_ld32(t_o + c * 32, o);
+        tc::tmem_ld32(t_o + c * 32, v);
         tc::tmem_ld_wait();
 #pragma unroll
-        for (int u = 0; u < 32; ++u) o[u] *= a;
-        tc::tmem_st32(t_o + c * 32, o);
+        for (int u = 0; u < 32; ++u) v[u] *= a;
+        tc::tmem_st32(t_o + c * 32, v);
       }
     }
-    // pass 2: p = exp2(s * log2e / sqrt(d) - m), bf16 P into S's columns
+    // pass 2: p = exp2(s * log2e / sqrt(d) - m) -> bf16 pairs written over
+    // the S columns already consumed (P cols [16q, 16q+16) <- S cols [32q, 32q+32))
     float sum = 0.f;
 #pragma unroll
-    for (int hf = 0; hf < 2; ++hf) {
-      tc::tmem_ld32(t_s + hf * 64, v);
-      tc::tmem_ld32(t_s + hf * 64 + 32, v + 32);
+    for (int q = 0; q < 4; ++q) {
+      tc::tmem_ld32(t_s + q * 32, v);
       tc::tmem_ld_wait();
       if (masked) {
 #pragma unroll
-        for (int c = 0; c < 64; ++c)
-          if (j0 + hf * 64 + c > hz) v[c] = -INFINITY;
+        for (int c = 0; c < 32; ++c)
+          if (j0 + q * 32 + c > hz) v[c] = -INFINITY;
       }
-      uint32_t pk[32];
+      uint32_t pk[16];
 #pragma unroll
-      for (int c = 0; c < 64; c += 2) {
+      for (int c = 0; c < 32; c += 2) {
         // 3 of every 4 pairs on the MUFU (ex2.approx.ftz(-inf) = +0), 1 on the FMA pipe
         const float x0 = fmaf(v[c], scale_log2, -mb), x1 = fmaf(v[c + 1], scale_log2, -mb);
         const bool poly = ((c >> 1) & 3) == 3;
@@ -140,8 +138,7 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
         sum += e0 + e1;
         pk[c / 2] = tc::pack_bf16(e0, e1);
       }
-      tc::tmem_st16(t_s + hf * 32, pk);
-      tc::tmem_st16(t_s + hf * 32 + 16, pk + 16);
+      tc::tmem_st16(t_s + q * 16, pk);
     }
     l = l * alpha + sum;
     tc::tmem_st_wait();
@@ -228,7 +225,6 @@ __global__ void __launch_bounds__(384, 1)
   const int nblk = max(nA, nB);
 
   if (warp < 4) {
-    tc::reg_dealloc<56>();
     if (warp == 0 && lane == 0) {
       tc::tma_prefetch(&tm_q);
       tc::tma_prefetch(&tm_k);
@@ -311,7 +307,6 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else {
-    tc::reg_alloc<208>();
     const int x = (warp - 4) >> 2;  // 0: tile A (warps 4-7), 1: tile B (warps 8-11)
     const int nx = x == 0 ? nA : nB;
     const int tx = x == 0 ? tA : tB;

@@ -235,3 +235,28 @@ def test_tc_scorer_gqa_dh128_vs_simt_and_oracle(cuda):
     np.testing.assert_array_equal(P.select_topk(tc, sel.size).cpu().numpy(), sel)
     res = P.run_selection(dw, chunks, cache, prompt, P.SelectionConfig(ratio=0.15, norm_layer=2))
     np.testing.assert_array_equal(res.selected_numpy(), sel)
+
+
+@pytest.mark.parametrize("precision", ["bf16", "f32"])
+def test_first_token_over_recomputed_cache(cuda, precision):
+    """Decode step over the recomputed cache (harness.py:458-469) vs the
+    oracle's forward on the same cache (its decode view)."""
+    P = _pkg()
+    dw, ow, g = _setup(P.c1_config(), 7, precision, P.SyntheticTask(**C1_TASK), 0)
+    kvs = [P.prefill_chunk(dw, c) for c in g.chunks]
+    cache = P.assemble(kvs)
+    before = P.first_token_logits(dw, cache, g.prompt_token_ids)  # stale cache, decode view on the fly
+    oc = oracle_cache(cache)
+    dk, dv = O.decode_view(oc, dw.config.rope_base)
+    n = oc.context_length
+    want0 = O.decoder_forward(ow, g.prompt_token_ids, n + np.arange(32),
+                              prefix=[(dk[l, :n], dv[l, :n]) for l in range(dk.shape[0])]).logits
+    assert rel_err(before.double().cpu().numpy(), want0) <= 1e-4
+    res = P.run_selection(dw, g.chunks, cache, g.prompt_token_ids, P.SelectionConfig(ratio=0.15))
+    out = P.recompute_selected(dw, cache, P.make_plan(cache, res.selected))
+    logits = P.first_token_logits(dw, out, g.prompt_token_ids)
+    oc2 = oracle_cache(out)
+    want = O.decoder_forward(ow, g.prompt_token_ids, n + np.arange(32),
+                             prefix=[(oc2.keys[l, :n], oc2.values[l, :n]) for l in range(oc2.n_layers)]).logits
+    assert rel_err(logits.double().cpu().numpy(), want) <= 1e-4
+    assert P.greedy_token(logits) == int(np.argmax(want))
