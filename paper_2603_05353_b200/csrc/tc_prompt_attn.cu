@@ -168,26 +168,20 @@ __global__ void __launch_bounds__(192, 1)
     float* T = reinterpret_cast<float*>(sm.v[0]);  // mode 1 transpose, [key][row ^ (key & 31)]
     for (int j = 0; j < nblk; ++j) {
       const int nk = min(128, it.n_keys - j * 128);
-      float v[64];
-      float s2[64];
+      float v[128];
       tc::mbar_wait(&sm.s_full, j & 1);
       tc::tc_fence_after();
-      tc::tmem_ld32(tmem + lane_off + kColS, v);
-      tc::tmem_ld32(tmem + lane_off + kColS + 32, v + 32);
-      tc::tmem_ld32(tmem + lane_off + kColS + 64, s2);
-      tc::tmem_ld32(tmem + lane_off + kColS + 96, s2 + 32);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) tc::tmem_ld32(tmem + lane_off + kColS + 32 * q, v + 32 * q);
       tc::tmem_ld_wait();
       tc::tc_fence_before();
-      tc::mbar_arrive(&sm.s_free);
+      tc::mbar_arrive(&sm.s_free);  // S may be overwritten by S(j+1) from here on
 #pragma unroll
-      for (int c = 0; c < 64; ++c) {
-        v[c] = c < nk ? v[c] * scale : -INFINITY;
-        s2[c] = c + 64 < nk ? s2[c] * scale : -INFINITY;
-      }
+      for (int c = 0; c < 128; ++c) v[c] = c < nk ? v[c] * scale : -INFINITY;
       if (mode == 0) {
         float mx = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < 64; ++c) mx = tc::max3(mx, v[c], s2[c]);
+        for (int c = 0; c < 128; c += 2) mx = tc::max3(mx, v[c], v[c + 1]);
         float alpha = 1.f;
         bool need = false;
         if (m_used == -INFINITY || mx - m_used > kRescale) {
@@ -195,45 +189,47 @@ __global__ void __launch_bounds__(192, 1)
           alpha = m_used == -INFINITY ? 0.f : expf(m_used - mx);
           m_used = mx;
         }
+        float sum = 0.f;
+#pragma unroll
+        for (int c = 0; c < 128; ++c) {
+          v[c] = expf(v[c] - m_used);
+          sum += v[c];
+        }
         // P(j-1) consumed and O = PV(0..j-1) complete
         if (j > 0) tc::mbar_wait(&sm.pv_done, (j - 1) & 1);
         tc::tc_fence_after();
         if (j > 0 && __any_sync(0xffffffffu, need)) {
           const float a = need ? alpha : 1.f;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            float o[32];
-            tc::tmem_ld32(tmem + lane_off + kColO + c * 32, o);
+#pragma unroll 1
+          for (int c = 0; c < 8; ++c) {
+            float o[16];
+            tc::tmem_ld16(tmem + lane_off + kColO + c * 16, o);
             tc::tmem_ld_wait();
 #pragma unroll
-            for (int u = 0; u < 32; ++u) o[u] *= a;
-            tc::tmem_st32(tmem + lane_off + kColO + c * 32, o);
+            for (int u = 0; u < 16; ++u) o[u] *= a;
+            tc::tmem_st16(tmem + lane_off + kColO + c * 16, reinterpret_cast<const uint32_t*>(o));
           }
         }
-        float sum = 0.f;
+        // P = hi + mid + lo (bf16 pairs), term t at TMEM cols kColP + 64 t + key / 2
 #pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-          float* e = hf == 0 ? v : s2;
+        for (int q = 0; q < 4; ++q) {
+          uint32_t p0[16], p1[16], p2[16];
 #pragma unroll
-          for (int c = 0; c < 64; ++c) {
-            e[c] = expf(e[c] - m_used);
-            sum += e[c];
+          for (int u = 0; u < 16; ++u) {
+            __nv_bfloat16 a0, a1, a2, b0, b1, b2;
+            split3(v[32 * q + 2 * u], a0, a1, a2);
+            split3(v[32 * q + 2 * u + 1], b0, b1, b2);
+            __nv_bfloat162 x0, x1, x2;
+            x0.x = a0; x0.y = b0;
+            x1.x = a1; x1.y = b1;
+            x2.x = a2; x2.y = b2;
+            p0[u] = *reinterpret_cast<uint32_t*>(&x0);
+            p1[u] = *reinterpret_cast<uint32_t*>(&x1);
+            p2[u] = *reinterpret_cast<uint32_t*>(&x2);
           }
-#pragma unroll
-          for (int t = 0; t < 3; ++t) {
-            uint32_t pk[32];
-#pragma unroll
-            for (int u = 0; u < 32; ++u) {
-              __nv_bfloat16 a0, a1, a2, b0, b1, b2;
-              split3(e[2 * u], a0, a1, a2);
-              split3(e[2 * u + 1], b0, b1, b2);
-              __nv_bfloat162 pr;
-              pr.x = t == 0 ? a0 : (t == 1 ? a1 : a2);
-              pr.y = t == 0 ? b0 : (t == 1 ? b1 : b2);
-              pk[u] = *reinterpret_cast<uint32_t*>(&pr);
-            }
-            tc::tmem_st32(tmem + lane_off + kColP + t * 64 + hf * 32, reinterpret_cast<float*>(pk));
-          }
+          tc::tmem_st16(tmem + lane_off + kColP + 0 * 64 + 16 * q, p0);
+          tc::tmem_st16(tmem + lane_off + kColP + 1 * 64 + 16 * q, p1);
+          tc::tmem_st16(tmem + lane_off + kColP + 2 * 64 + 16 * q, p2);
         }
         l = l * alpha + sum;
         tc::tmem_st_wait();
@@ -243,12 +239,7 @@ __global__ void __launch_bounds__(192, 1)
         // p = exp(s - m_final) / l_final -> transposed smem -> column sums
         asm volatile("bar.sync 1, 128;" ::: "memory");  // previous block's column reads done
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          const float p0 = valid ? expf(v[c] - mf) * inv_lf : 0.f;
-          const float p1 = valid ? expf(s2[c] - mf) * inv_lf : 0.f;
-          T[c * 128 + (row ^ (c & 31))] = p0;
-          T[(c + 64) * 128 + (row ^ (c & 31))] = p1;
-        }
+        for (int c = 0; c < 128; ++c) T[c * 128 + (row ^ (c & 31))] = valid ? expf(v[c] - mf) * inv_lf : 0.f;
         asm volatile("bar.sync 1, 128;" ::: "memory");
         const int c = row;  // this thread sums key column c over the tile rows
         float acc = 0.f;

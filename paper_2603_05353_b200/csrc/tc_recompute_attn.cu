@@ -80,20 +80,21 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
     tc::tc_fence_after();
     const int j0 = j * kKeys;
     const bool masked = __any_sync(0xffffffffu, j0 + kKeys - 1 > hz);
-    float v[32];
-    // pass 1: row max over the block, 32 columns at a time
+    float v[64];
+    // pass 1: row max over the block (two 64-column halves)
     float mx = -INFINITY;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      tc::tmem_ld32(t_s + q * 32, v);
+    for (int hf = 0; hf < 2; ++hf) {
+      tc::tmem_ld32(t_s + hf * 64, v);
+      tc::tmem_ld32(t_s + hf * 64 + 32, v + 32);
       tc::tmem_ld_wait();
       if (masked) {
 #pragma unroll
-        for (int c = 0; c < 32; ++c)
-          if (j0 + q * 32 + c > hz) v[c] = -INFINITY;
+        for (int c = 0; c < 64; ++c)
+          if (j0 + hf * 64 + c > hz) v[c] = -INFINITY;
       }
 #pragma unroll
-      for (int c = 0; c < 32; c += 2) mx = tc::max3(mx, v[c], v[c + 1]);
+      for (int c = 0; c < 64; c += 2) mx = tc::max3(mx, v[c], v[c + 1]);
     }
     float alpha = 1.f;
     bool need = false;
@@ -116,20 +117,21 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
       }
     }
     // pass 2: p = exp2(s * log2e / sqrt(d) - m) -> bf16 pairs written over
-    // the S columns already consumed (P cols [16q, 16q+16) <- S cols [32q, 32q+32))
+    // the consumed S columns (P cols [32 hf, 32 hf + 32) <- S cols [64 hf, 64 hf + 64))
     float sum = 0.f;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      tc::tmem_ld32(t_s + q * 32, v);
+    for (int hf = 0; hf < 2; ++hf) {
+      tc::tmem_ld32(t_s + hf * 64, v);
+      tc::tmem_ld32(t_s + hf * 64 + 32, v + 32);
       tc::tmem_ld_wait();
       if (masked) {
 #pragma unroll
-        for (int c = 0; c < 32; ++c)
-          if (j0 + q * 32 + c > hz) v[c] = -INFINITY;
+        for (int c = 0; c < 64; ++c)
+          if (j0 + hf * 64 + c > hz) v[c] = -INFINITY;
       }
-      uint32_t pk[16];
+      uint32_t pk[32];
 #pragma unroll
-      for (int c = 0; c < 32; c += 2) {
+      for (int c = 0; c < 64; c += 2) {
         // 3 of every 4 pairs on the MUFU (ex2.approx.ftz(-inf) = +0), 1 on the FMA pipe
         const float x0 = fmaf(v[c], scale_log2, -mb), x1 = fmaf(v[c + 1], scale_log2, -mb);
         const bool poly = ((c >> 1) & 3) == 3;
@@ -138,7 +140,8 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
         sum += e0 + e1;
         pk[c / 2] = tc::pack_bf16(e0, e1);
       }
-      tc::tmem_st16(t_s + q * 16, pk);
+      tc::tmem_st16(t_s + hf * 32, pk);
+      tc::tmem_st16(t_s + hf * 32 + 16, pk + 16);
     }
     l = l * alpha + sum;
     tc::tmem_st_wait();
@@ -153,8 +156,8 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
   const float inv = l > 0.f ? 1.f / l : 0.f;
   const int64_t orow = (int64_t)tok * H + g * G + row % G;
   __nv_bfloat16* dst = out + orow * kDh;
-  if (ml_out && valid) {
-    ml_out[2 * orow] = m_used;
+  if (ml_out && valid) {  // (max, sum) in natural units of the scaled logits, like the SIMT kernel
+    ml_out[2 * orow] = m_used == -INFINITY ? -INFINITY : m_used * scale_log2 * 0.6931471805599453f;
     ml_out[2 * orow + 1] = l;
   }
 #pragma unroll

@@ -183,6 +183,14 @@ def test_recompute_attention_unsorted_and_empty_horizons(T, cuda, partial):
         assert np.all(ml[:7, :, 1] == 0) and np.all(np.isneginf(ml[:7, :, 0]))
         assert np.all(out[:7].float().cpu().numpy() == 0)
         rows = slice(7, None)
+        # (max, sum) in natural units of the scaled logits: l * e^m == sum_j e^(s_j)
+        qd, kd = q.double().cpu().numpy()[7:], k.double().cpu().numpy()
+        for i in (0, 100, 300):
+            r = 7 + i
+            for h in (0, 13):
+                s_ = qd[i, h] @ kd[: hz[r] + 1, h // (H // hkv)].T / np.sqrt(dh)
+                mt = s_.max()
+                assert ml[r, h, 1] * np.exp(ml[r, h, 0] - mt) == pytest.approx(np.exp(s_ - mt).sum(), rel=2e-2)
     else:
         out = E.recompute_attn(q, k, v, hzt, H, hkv, dh)
         rows = slice(0, None)
