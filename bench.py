@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="one warm step inside cudaProfilerStart/Stop, then exit")
+    ap.add_argument("--simulate-ranks", type=int, default=1,
+                    help="run the chunk-sharded path with R ranks as threads on one GPU (functional check)")
     return ap.parse_args()
 
 
@@ -290,6 +292,93 @@ def run_ours(args, world, rank, local):
 
 
 # ---------------------------------------------------------------------------
+# N GPUs: one context chunk-sharded across ranks, strong scaling
+# ---------------------------------------------------------------------------
+
+
+def run_sharded(args, comm, world, rank, sync):
+    """Every rank holds the chunks it owns (zig-zag), scores them, merges the
+    per-layer softmax states and the top-k candidates with the other ranks,
+    and recomputes its own selected tokens with attention over all ranks'
+    keys.  value = context tokens / step time (max over ranks)."""
+    import torch
+
+    import paper_2603_05353_b200 as P
+    from paper_2603_05353_b200 import sharding as SH
+
+    cfg = P.llama3_8b_config()
+    if args.layers != 32:
+        import dataclasses
+
+        cfg = dataclasses.replace(cfg, n_layers=args.layers)
+    weights = P.DeviceWeights.random(cfg, seed=7, precision="bf16")
+    task = P.SyntheticTask(kind="uniform_noise", total_length=args.ctx, fixed_size=args.chunk, prompt_length=32,
+                           vocab_size=cfg.vocab_size)
+    gen = P.generate_task(task, seed=0)
+    chunks, prompt = gen.chunks, gen.prompt_token_ids
+    shard = SH.make_shard([c.local_length for c in chunks], rank, world)
+    my_kvs = [P.prefill_chunk(weights, chunks[c]) for c in shard.chunk_ids]
+    sel_cfg = P.SelectionConfig(ratio=args.ratio)
+    n_ctx = sum(c.local_length for c in chunks)
+
+    def step(prompt_ids):
+        local = P.assemble(my_kvs)
+        res = SH.sharded_select(weights, shard, local, prompt_ids, sel_cfg, comm)
+        SH.sharded_recompute(weights, shard, local, res.selected, comm)
+        return res
+
+    for _ in range(args.warmup):
+        res = step(prompt)
+    torch.cuda.synchronize()
+    sync()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        res = step(prompt)
+    ev1.record()
+    torch.cuda.synchronize()
+    sync()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    ms_all = comm.all_gather(torch.tensor([ms], dtype=torch.float64, device="cuda"))
+    ms = max(float(x.item()) for x in ms_all)
+    # e2e: host prompt ids in, selected indices out, through the sharded API
+    times = []
+    for _ in range(max(2, min(args.steps, 3))):
+        torch.cuda.synchronize()
+        sync()
+        t0 = time.perf_counter()
+        res = step(np.array(prompt))
+        sel_host = res.selected.cpu().numpy()
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    e2e_all = comm.all_gather(torch.tensor([statistics.median(times) * 1e3], dtype=torch.float64, device="cuda"))
+    e2e_ms = max(float(x.item()) for x in e2e_all)
+    return {
+        "metric": METRIC,
+        "value": n_ctx / (ms / 1e3),
+        "unit": "ctx tok/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (reference generate_task uniform_noise tokens; random-init weights)",
+        "config": {"workload": f"C2 chunk-sharded over {world} ranks (zig-zag chunk ownership, NCCL softmax-state "
+                               f"merges + top-k candidate all-gather + sparse-query partial attention all-to-all)",
+                   "ctx_tokens": n_ctx, "chunks": len(chunks), "recompute_ratio": args.ratio,
+                   "selected": int(sel_host.size), "parallelism": f"chunk-sharded x{world}",
+                   "l2": "inputs larger than L2"},
+        "e2e": {"value": n_ctx / (e2e_ms / 1e3), "unit": "ctx tok/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": int(prompt.nbytes), "d2h_bytes_per_step": int(sel_host.size * 8)},
+        "roofline": None,
+        "gpu_launches": None,
+    }
+
+
+# ---------------------------------------------------------------------------
 # CPU baseline: the oracle (NumPy port of the reference) on a bounded sample
 # ---------------------------------------------------------------------------
 
@@ -405,6 +494,32 @@ def main():
             print(json.dumps(line), flush=True)
         return
     world, rank, local = dist_setup()
+    if world > 1:
+        from paper_2603_05353_b200.sharding import TorchComm
+
+        import torch.distributed as dist
+
+        line = run_sharded(args, TorchComm(), world, rank, dist.barrier)
+        clk = None
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+        dist.destroy_process_group()
+        return
+    if args.simulate_ranks > 1:
+        from paper_2603_05353_b200.sharding import ThreadComm
+
+        import torch
+
+        def body(comm):
+            return run_sharded(args, comm, comm.world, comm.rank,
+                               lambda: comm.all_gather(torch.zeros(1, device="cuda")))
+
+        line = ThreadComm.run(args.simulate_ranks, body)[0]
+        line["n_gpus"] = 1
+        line["simulated_ranks"] = args.simulate_ranks
+        line["scaling"] = "none (ranks simulated as threads on one GPU: functional check, not a scaling number)"
+        print(json.dumps(line), flush=True)
+        return
     line = run_ours(args, world, rank, local)
     if line is None:
         return

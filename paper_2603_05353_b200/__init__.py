@@ -51,6 +51,7 @@ from .selection import (
     select_random,
     select_topk,
 )
+from .storage import load_cache, save_cache
 from .tasks import GeneratedTask, SyntheticTask, generate_task, make_chunks
 
 __version__ = "0.1.0"

@@ -57,36 +57,39 @@ def _digest(paths) -> str:
     return h.hexdigest()
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile all kernels; skip when sources and flags are unchanged."""
+def build(force: bool = False, verbose: bool = False, out_dir: Path = OUT_DIR, extra_flags=()) -> Path:
+    """Compile all kernels; skip when sources and flags are unchanged.
+    ``out_dir`` / ``extra_flags`` build kernel variants for A/B timing."""
+    out_dir = Path(out_dir)
+    lib = out_dir / "libifkv.so"
     deps = list(_sources()) + list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h"))
-    stamp = OUT_DIR / "libifkv.sha256"
-    digest = _digest(deps)
-    if not force and LIB.exists() and stamp.exists() and stamp.read_text() == digest:
-        return LIB
-    OUT_DIR.mkdir(parents=True, exist_ok=True)
+    stamp = out_dir / "libifkv.sha256"
+    digest = _digest(deps) + " ".join(extra_flags)
+    if not force and lib.exists() and stamp.exists() and stamp.read_text() == digest:
+        return lib
+    out_dir.mkdir(parents=True, exist_ok=True)
     nvcc = _nvcc()
     objs = []
 
     def compile_one(src: Path):
-        obj = OUT_DIR / (src.stem + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+        obj = out_dir / (src.stem + ".o")
+        cmd = [nvcc, *NVCC_FLAGS, *extra_flags, "-c", str(src), "-o", str(obj)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src.name}:\n{res.stdout}\n{res.stderr}")
-        (OUT_DIR / (src.stem + ".ptxas.txt")).write_text(res.stderr)
+        (out_dir / (src.stem + ".ptxas.txt")).write_text(res.stderr)
         return obj
 
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as pool:
         objs = list(pool.map(compile_one, _sources()))
-    cmd = [nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs)]
+    cmd = [nvcc, *ARCH, "-shared", "-o", str(lib), *map(str, objs)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
     stamp.write_text(digest)
     if verbose:
-        print(f"built {LIB}", file=sys.stderr)
-    return LIB
+        print(f"built {lib}", file=sys.stderr)
+    return lib
 
 
 if __name__ == "__main__":

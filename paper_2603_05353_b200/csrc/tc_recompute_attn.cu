@@ -38,6 +38,15 @@ constexpr int kPanel = 128 * 128;
 constexpr int kTile = 2 * kPanel;
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleLog2 = 8.0f;
+// A/B switches (tools/attn_bench.py): register split between the producer /
+// MMA warpgroup and the softmax warpgroups; which exp2 pairs use the FMA-pipe
+// polynomial (pair index & 3 == kPolyPair; -1 = none).
+#ifndef IFKV_ATTN_SETMAXNREG
+#define IFKV_ATTN_SETMAXNREG 0
+#endif
+#ifndef IFKV_ATTN_POLY_PAIR
+#define IFKV_ATTN_POLY_PAIR 3
+#endif
 
 struct Smem {
   uint8_t q[2][kTile];
@@ -134,7 +143,7 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
       for (int c = 0; c < 64; c += 2) {
         // 3 of every 4 pairs on the MUFU (ex2.approx.ftz(-inf) = +0), 1 on the FMA pipe
         const float x0 = fmaf(v[c], scale_log2, -mb), x1 = fmaf(v[c + 1], scale_log2, -mb);
-        const bool poly = ((c >> 1) & 3) == 3;
+        const bool poly = ((c >> 1) & 3) == IFKV_ATTN_POLY_PAIR;
         const float e0 = poly ? tc::ex2_poly(x0) : tc::ex2(x0);
         const float e1 = poly ? tc::ex2_poly(x1) : tc::ex2(x1);
         sum += e0 + e1;
@@ -228,6 +237,9 @@ __global__ void __launch_bounds__(384, 1)
   const int nblk = max(nA, nB);
 
   if (warp < 4) {
+#if IFKV_ATTN_SETMAXNREG
+    tc::reg_dealloc<96>();
+#endif
     if (warp == 0 && lane == 0) {
       tc::tma_prefetch(&tm_q);
       tc::tma_prefetch(&tm_k);
@@ -310,6 +322,9 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else {
+#if IFKV_ATTN_SETMAXNREG
+    tc::reg_alloc<200>();
+#endif
     const int x = (warp - 4) >> 2;  // 0: tile A (warps 4-7), 1: tile B (warps 8-11)
     const int nx = x == 0 ? nA : nB;
     const int tx = x == 0 ? tA : tB;

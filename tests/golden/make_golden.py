@@ -96,6 +96,17 @@ def tiny_case(out):
     for mode in ("mean", "max"):
         imps, _ = ck.score_chunks(w, chunks, prompt, budget=6, chunk_score=mode, prefilled=kvs)
         out[f"tiny_imp_{mode}"] = imps
+    # IFKC files written by the reference (f64 and f32 precision codes)
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as d:
+        ck.save_cache(kvs[1], Path(d) / "a.ifkc")
+        out["tiny_ifkc_f64"] = np.frombuffer((Path(d) / "a.ifkc").read_bytes(), dtype=np.uint8)
+        w32 = ck.init_weights(cfg, seed=3, precision="f32")
+        c32 = ck.prefill_chunk(w32, ck.ChunkSpec("f32chunk", np.arange(5)))
+        ck.save_cache(c32, Path(d) / "b.ifkc")
+        out["tiny_ifkc_f32"] = np.frombuffer((Path(d) / "b.ifkc").read_bytes(), dtype=np.uint8)
+        out["tiny_ifkc_f32_keys"] = np.stack(c32.keys)
 
 
 def c1_case(out, seed):
