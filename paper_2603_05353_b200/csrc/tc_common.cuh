@@ -177,6 +177,39 @@ __device__ __forceinline__ float ex2_poly(float x) {
   return x < -126.f ? 0.f : r;  // masked (-inf) and underflowing inputs give exactly 0, like ex2.approx.ftz
 }
 
+// Packed fp32x2 arithmetic (sm_100 FFMA2 / FADD2: two lanes of work per
+// FMA-pipe issue).
+__device__ __forceinline__ unsigned long long f2_as_u64(float2 v) {
+  return (unsigned long long)__float_as_uint(v.x) | ((unsigned long long)__float_as_uint(v.y) << 32);
+}
+__device__ __forceinline__ float2 u64_as_f2(unsigned long long u) {
+  return make_float2(__uint_as_float((uint32_t)u), __uint_as_float((uint32_t)(u >> 32)));
+}
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_as_u64(a)), "l"(f2_as_u64(b)), "l"(f2_as_u64(c)));
+  return u64_as_f2(d);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_as_u64(a)), "l"(f2_as_u64(b)));
+  return u64_as_f2(d);
+}
+// ex2_poly on a pair with packed arithmetic (same polynomial, same exactness
+// for masked inputs).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  const float2 xc = make_float2(fmaxf(x.x, -126.f), fmaxf(x.y, -126.f));
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = fadd2(xc, magic);
+  const float2 f = fadd2(xc, fadd2(magic, make_float2(-t.x, -t.y)));
+  float2 p = ffma2(make_float2(0.05295114f, 0.05295114f), f, make_float2(0.24165066f, 0.24165066f));
+  p = ffma2(p, f, make_float2(0.69353656f, 0.69353656f));
+  p = ffma2(p, f, make_float2(1.f, 1.f));
+  const float r0 = __int_as_float(__float_as_int(t.x) * 8388608 + __float_as_int(p.x));
+  const float r1 = __int_as_float(__float_as_int(t.y) * 8388608 + __float_as_int(p.y));
+  return make_float2(x.x < -126.f ? 0.f : r0, x.y < -126.f ? 0.f : r1);
+}
+
 __device__ __forceinline__ float max3(float a, float b, float c) {
   float d;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));

@@ -39,13 +39,13 @@ constexpr int kTile = 2 * kPanel;
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleLog2 = 8.0f;
 // A/B switches (tools/attn_bench.py): register split between the producer /
-// MMA warpgroup and the softmax warpgroups; which exp2 pairs use the FMA-pipe
-// polynomial (pair index & 3 == kPolyPair; -1 = none).
+// MMA warpgroup and the softmax warpgroups; which exp2 pairs go to the
+// FMA-pipe polynomial instead of the MUFU: bit (pair index & 7) of the mask.
 #ifndef IFKV_ATTN_SETMAXNREG
 #define IFKV_ATTN_SETMAXNREG 0
 #endif
-#ifndef IFKV_ATTN_POLY_PAIR
-#define IFKV_ATTN_POLY_PAIR 3
+#ifndef IFKV_ATTN_POLY_MASK
+#define IFKV_ATTN_POLY_MASK 0x00
 #endif
 
 struct Smem {
@@ -139,16 +139,23 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
           if (j0 + hf * 64 + c > hz) v[c] = -INFINITY;
       }
       uint32_t pk[32];
+      const float2 sc2 = make_float2(scale_log2, scale_log2), mb2 = make_float2(-mb, -mb);
+      float2 sum2 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int c = 0; c < 64; c += 2) {
-        // 3 of every 4 pairs on the MUFU (ex2.approx.ftz(-inf) = +0), 1 on the FMA pipe
-        const float x0 = fmaf(v[c], scale_log2, -mb), x1 = fmaf(v[c + 1], scale_log2, -mb);
-        const bool poly = ((c >> 1) & 3) == IFKV_ATTN_POLY_PAIR;
-        const float e0 = poly ? tc::ex2_poly(x0) : tc::ex2(x0);
-        const float e1 = poly ? tc::ex2_poly(x1) : tc::ex2(x1);
-        sum += e0 + e1;
-        pk[c / 2] = tc::pack_bf16(e0, e1);
+        // packed x = s * scale - m; exp2 on the MUFU, or on the FMA pipe for
+        // the pairs selected by IFKV_ATTN_POLY_MASK (ex2.approx.ftz(-inf) = +0)
+        const float2 xx = tc::ffma2(make_float2(v[c], v[c + 1]), sc2, mb2);
+        float2 e;
+        if ((IFKV_ATTN_POLY_MASK >> ((c >> 1) & 7)) & 1) {
+          e = tc::ex2_poly2(xx);
+        } else {
+          e = make_float2(tc::ex2(xx.x), tc::ex2(xx.y));
+        }
+        sum2 = tc::fadd2(sum2, e);
+        pk[c / 2] = tc::pack_bf16(e.x, e.y);
       }
+      sum += sum2.x + sum2.y;
       tc::tmem_st16(t_s + hf * 32, pk);
       tc::tmem_st16(t_s + hf * 32 + 16, pk + 16);
     }

@@ -43,7 +43,7 @@ def run(lib, iters=30):
 
 if __name__ == "__main__":
     libs = sys.argv[1:] or [str(ROOT / "paper_2603_05353_b200/_build/libifkv.so")]
-    for rep in range(2):
+    for rep in range(4):
         for lib in libs:
             ms, tf = run(lib)
             print(f"{lib}: {ms:.3f} ms  {tf:.0f} TFLOP/s", flush=True)
