@@ -52,7 +52,9 @@ def parse():
     ap.add_argument("--ctx", type=int, default=32768)
     ap.add_argument("--chunk", type=int, default=2048)
     ap.add_argument("--ratio", type=float, default=0.15)
-    ap.add_argument("--layers", type=int, default=32, help="override model depth (debug only)")
+    ap.add_argument("--layers", type=int, default=0, help="override model depth (debug only)")
+    ap.add_argument("--model", choices=["llama3_8b", "qwen25vl_7b"], default="llama3_8b")
+    ap.add_argument("--reorder", action="store_true", help="information-flow chunk reordering (config 3)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="one warm step inside cudaProfilerStart/Stop, then exit")
@@ -134,6 +136,49 @@ def max_over_ranks(x: float, world: int) -> float:
 
 
 # ---------------------------------------------------------------------------
+# workloads (BASELINE.json configs)
+# ---------------------------------------------------------------------------
+
+
+def model_config(args):
+    import dataclasses
+
+    import paper_2603_05353_b200 as P
+
+    cfg = P.llama3_8b_config() if args.model == "llama3_8b" else P.qwen25vl_7b_config()
+    if args.layers:
+        cfg = dataclasses.replace(cfg, n_layers=args.layers)
+    return cfg
+
+
+def make_task(args, cfg):
+    """C2/C3: fixed-size chunks; C4 (Qwen2.5-VL): 24 image-token chunks of
+    1280 followed by 512-token text chunks up to the context length."""
+    import paper_2603_05353_b200 as P
+
+    if args.model == "qwen25vl_7b":
+        lens = [1280] * 24
+        while sum(lens) < args.ctx:
+            lens.append(min(512, args.ctx - sum(lens)))
+        cuts = tuple(np.cumsum(lens)[:-1].tolist())
+        return P.SyntheticTask(kind="uniform_noise", total_length=sum(lens), fixed_size=None, boundaries=cuts,
+                               prompt_length=32, vocab_size=cfg.vocab_size)
+    return P.SyntheticTask(kind="uniform_noise", total_length=args.ctx, fixed_size=args.chunk, prompt_length=32,
+                           vocab_size=cfg.vocab_size)
+
+
+def workload_name(args, cfg, n_ctx, n_chunks, k):
+    import paper_2603_05353_b200 as P
+
+    base = "C2: Llama-3-8B shape" if args.model == "llama3_8b" else "C4: Qwen2.5-VL-7B LM shape"
+    if args.reorder:
+        base = base.replace("C2", "C3") + " + info-flow reorder"
+    return (f"{base} ({cfg.n_layers}L, {cfg.n_heads}q/{cfg.kv_heads}kv heads, d_ff {cfg.d_ff}), {n_ctx} ctx in "
+            f"{n_chunks} chunks, 32-token prompt, {args.ratio:.0%} recompute (k={k}), norm layer "
+            f"{P.default_norm_layer(cfg.n_layers)}")
+
+
+# ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
 
@@ -145,14 +190,9 @@ def run_ours(args, world, rank, local):
     from paper_2603_05353_b200 import _native as N
     from paper_2603_05353_b200 import engine as E
 
-    cfg = P.llama3_8b_config()
-    if args.layers != 32:
-        import dataclasses
-
-        cfg = dataclasses.replace(cfg, n_layers=args.layers)
+    cfg = model_config(args)
     weights = P.DeviceWeights.random(cfg, seed=7, precision="bf16")
-    task = P.SyntheticTask(kind="uniform_noise", total_length=args.ctx, fixed_size=args.chunk, prompt_length=32,
-                           vocab_size=cfg.vocab_size)
+    task = make_task(args, cfg)
     gen = P.generate_task(task, seed=rank)
     chunks, prompt = gen.chunks, gen.prompt_token_ids
     chunk_kvs = [P.prefill_chunk(weights, c) for c in chunks]  # prepared context (not timed)
@@ -161,7 +201,8 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize()
 
     def step(timer=None):
-        return P.assemble_select_recompute(weights, chunk_kvs, chunks, prompt, sel_cfg, timer=timer)
+        return P.assemble_select_recompute(weights, chunk_kvs, chunks, prompt, sel_cfg, reorder=args.reorder,
+                                           timer=timer)
 
     for _ in range(args.warmup):
         res = step()
@@ -218,7 +259,8 @@ def run_ours(args, world, rank, local):
         for _ in range(max(2, min(args.steps, 5))):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            res = P.assemble_select_recompute(weights, chunk_kvs, chunks, np.array(prompt), sel_cfg)
+            res = P.assemble_select_recompute(weights, chunk_kvs, chunks, np.array(prompt), sel_cfg,
+                                              reorder=args.reorder)
             sel_host = res.selection.selected_numpy()
             sc_host = res.selection.scores_numpy()
             torch.cuda.synchronize()
@@ -232,7 +274,7 @@ def run_ours(args, world, rank, local):
 
     # roofline of the dominant kernel of ours: recompute attention (tensor-bound)
     H, Dh, L = cfg.n_heads, cfg.d_head, cfg.n_layers
-    flops_per_launch = 4.0 * H * Dh * float(np.sum(sel_h + 1))
+    flops_per_launch = 4.0 * H * Dh * float(np.sum(sel_h + 1))  # (selected in the final, permuted layout)
     attn_avg_ms = float(np.mean(attn_ms)) if attn_ms else None
     achieved = flops_per_launch / (attn_avg_ms / 1e3) / 1e12 if attn_avg_ms else None
     peak = PEAKS["bf16_tflops_sustained"]
@@ -241,7 +283,8 @@ def run_ours(args, world, rank, local):
             "peak_source": PEAKS["source"] + " sustained bf16",
             "algorithmic_flops_per_launch": flops_per_launch, "avg_launch_ms": attn_avg_ms,
             "launches_per_step": len(attn_ms), "share_of_step": float(np.sum(attn_ms)) / ms if attn_ms else None}
-    rot_bytes = 2.0 * n_ctx * L * cfg.kv_heads * Dh * 2 * (1 - args.chunk / n_ctx)  # first chunk has delta 0
+    moved = float(rot[0][2]) if rot else 0.0  # rows whose rotation delta is nonzero (chunk 0 has delta 0)
+    rot_bytes = 2.0 * moved * L * cfg.kv_heads * Dh * 2  # read + write K of every moved row, all layers
     rot_roof = None
     if rot_ms:
         ach = rot_bytes / (float(np.mean(rot_ms)) / 1e3) / 1e9
@@ -273,9 +316,7 @@ def run_ours(args, world, rank, local):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (reference generate_task uniform_noise tokens; random-init weights, GPU-drawn N(0,1)/sqrt(fan_in))",
-        "config": {"workload": f"C2: Llama-3-8B shape ({cfg.n_layers}L, 32q/8kv heads, d_ff 14336), {n_ctx} ctx = "
-                               f"{len(chunks)} x {args.chunk} chunks, 32-token prompt, {args.ratio:.0%} recompute "
-                               f"(k={sel_h.size}), norm layer {P.default_norm_layer(cfg.n_layers)}",
+        "config": {"workload": workload_name(args, cfg, n_ctx, len(chunks), sel_h.size),
                    "ctx_tokens": n_ctx, "chunks": len(chunks), "recompute_ratio": args.ratio,
                    "selected": int(sel_h.size), "parallelism": f"replicas x{world}",
                    "l2": "inputs larger than L2 (4.3 GB KV slab + 16 GB weights per step)"},
@@ -306,14 +347,9 @@ def run_sharded(args, comm, world, rank, sync):
     import paper_2603_05353_b200 as P
     from paper_2603_05353_b200 import sharding as SH
 
-    cfg = P.llama3_8b_config()
-    if args.layers != 32:
-        import dataclasses
-
-        cfg = dataclasses.replace(cfg, n_layers=args.layers)
+    cfg = model_config(args)
     weights = P.DeviceWeights.random(cfg, seed=7, precision="bf16")
-    task = P.SyntheticTask(kind="uniform_noise", total_length=args.ctx, fixed_size=args.chunk, prompt_length=32,
-                           vocab_size=cfg.vocab_size)
+    task = make_task(args, cfg)
     gen = P.generate_task(task, seed=0)
     chunks, prompt = gen.chunks, gen.prompt_token_ids
     shard = SH.make_shard([c.local_length for c in chunks], rank, world)
