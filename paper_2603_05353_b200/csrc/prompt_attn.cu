@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(256) prompt_attn_partial_kernel(
 // grid (G * H * M), Dh threads (<= 256): merge the group's items in order.
 // Items of group g: [item_begin[g], item_begin[g+1]) then, if
 // prompt_item0 >= 0, item prompt_item0 + g (the group's causal prompt item).
+// Two passes (max, then weighted sums) with 4 independent loads in flight.
 __global__ void prompt_attn_merge_kernel(const float* __restrict__ part_ml, const float* __restrict__ part_o,
                                          const int32_t* __restrict__ item_begin, int prompt_item0, int H, int M,
                                          int Dh, float* __restrict__ ctx, float* __restrict__ ml) {
@@ -131,19 +132,20 @@ __global__ void prompt_attn_merge_kernel(const float* __restrict__ part_ml, cons
   const int m = r % M, h = (r / M) % H, g = r / (M * H);
   const int b = item_begin[g], e = item_begin[g + 1];
   const int n = e - b + (prompt_item0 >= 0 ? 1 : 0);
-  auto item = [&](int k) { return k < e - b ? b + k : prompt_item0 + g; };
+  auto row_of = [&](int k) -> int64_t {
+    const int it = k < e - b ? b + k : prompt_item0 + g;
+    return ((int64_t)it * H + h) * M + m;
+  };
   float mx = -INFINITY;
-  for (int k = 0; k < n; ++k) {
-    float mi = part_ml[2 * (((int64_t)item(k) * H + h) * M + m)];
-    mx = fmaxf(mx, mi);
-  }
+#pragma unroll 4
+  for (int k = 0; k < n; ++k) mx = fmaxf(mx, part_ml[2 * row_of(k)]);
   float l = 0.f, o = 0.f;
   const int d = threadIdx.x;
+#pragma unroll 4
   for (int k = 0; k < n; ++k) {
-    int64_t row = ((int64_t)item(k) * H + h) * M + m;
-    float mi = part_ml[2 * row];
-    if (mi == -INFINITY) continue;
-    float a = expf(mi - mx);
+    const int64_t row = row_of(k);
+    const float mi = part_ml[2 * row];
+    const float a = mi == -INFINITY ? 0.f : expf(mi - mx);
     l += part_ml[2 * row + 1] * a;
     if (d < Dh) o += part_o[row * Dh + d] * a;
   }
