@@ -34,7 +34,7 @@ SIGNATURES = {
     "ifkv_split3": [P, I64, P, P],
     "ifkv_qkv_rope_scatter": [P, I32, I32, I32, I32, I32, I32, P, I32, P, P, P, P, P],
     "ifkv_prompt_attn_partial": [I32, P, P, P, P, P, P, I32, I32, I32, I32, I32, F32, P, P, P],
-    "ifkv_prompt_attn_merge": [P, P, P, I32, I32, I32, I32, I32, P, P, P],
+    "ifkv_prompt_attn_merge": [P, P, P, I32, I32, I32, I32, I32, P, P, P, P],
     "ifkv_prompt_attn_tc_supported": [I32, I32, I32, I32, I32],
     "ifkv_prompt_attn_partial_tc": [P, I32, P, P, I32, P, I32, I32, I32, I32, I32, F32, P, P, P],
     "ifkv_score_columns_tc": [P, I32, P, I32, P, I32, I32, P, I32, I32, I32, F32, P, P, P],
@@ -55,6 +55,8 @@ _lib = None
 def load(path: Path = LIB_PATH):
     """Load (once) and type the library; raise NativeError if it is absent."""
     global _lib
+    if _lib is not None:
+        return _lib
     with _lock:
         if _lib is not None:
             return _lib
@@ -71,6 +73,7 @@ def load(path: Path = LIB_PATH):
         lib.ifkv_last_error.restype = C.c_char_p
         lib.ifkv_abi_version.argtypes = []
         lib.ifkv_abi_version.restype = C.c_int
+        _fns.clear()
         _lib = lib
         return lib
 
@@ -78,14 +81,21 @@ def load(path: Path = LIB_PATH):
 LAUNCH_COUNT = [0]  # entry-point calls that enqueue kernels (bench gpu_launches)
 
 
+_fns: dict = {}
+
+
 def call(name: str, *args) -> int:
     """Invoke an entry point and translate its status code."""
-    lib = load()
-    if not name.endswith("_supported"):
+    fn = _fns.get(name)
+    if fn is None:
+        fn = _fns[name] = getattr(load(), name)
+    query = name.endswith("_supported")
+    if not query:
         LAUNCH_COUNT[0] += 1
-    status = getattr(lib, name)(*args)
-    if status == 0 or name.endswith("_supported"):
+    status = fn(*args)
+    if status == 0 or query:
         return status
+    lib = load()
     msg = lib.ifkv_last_error().decode(errors="replace")
     if status == 2:
         raise ConfigurationError(f"{name}: {msg}")

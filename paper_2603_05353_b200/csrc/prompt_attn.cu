@@ -127,7 +127,8 @@ __global__ void __launch_bounds__(256) prompt_attn_partial_kernel(
 // Two passes (max, then weighted sums) with 4 independent loads in flight.
 __global__ void prompt_attn_merge_kernel(const float* __restrict__ part_ml, const float* __restrict__ part_o,
                                          const int32_t* __restrict__ item_begin, int prompt_item0, int H, int M,
-                                         int Dh, float* __restrict__ ctx, float* __restrict__ ml) {
+                                         int Dh, float* __restrict__ ctx, float* __restrict__ ml,
+                                         __nv_bfloat16* __restrict__ ctx3, int64_t plane) {
   const int r = blockIdx.x;  // (g, h, m)
   const int m = r % M, h = (r / M) % H, g = r / (M * H);
   const int b = item_begin[g], e = item_begin[g + 1];
@@ -149,7 +150,18 @@ __global__ void prompt_attn_merge_kernel(const float* __restrict__ part_ml, cons
     l += part_ml[2 * row + 1] * a;
     if (d < Dh) o += part_o[row * Dh + d] * a;
   }
-  if (d < Dh) ctx[(((int64_t)g * M + m) * H + h) * Dh + d] = l > 0.f ? o / l : 0.f;  // no item: empty shard
+  const float c = l > 0.f ? o / l : 0.f;  // no item: empty shard
+  const int64_t ci = (((int64_t)g * M + m) * H + h) * Dh + d;
+  if (d < Dh) {
+    ctx[ci] = c;
+    if (ctx3) {  // fused hi/mid/lo split of the next GEMM's operand
+      __nv_bfloat16 a0, a1, a2;
+      split3(c, a0, a1, a2);
+      ctx3[ci] = a0;
+      ctx3[plane + ci] = a1;
+      ctx3[2 * plane + ci] = a2;
+    }
+  }
   if (d == 0) {
     ml[2 * (((int64_t)g * H + h) * M + m)] = mx;
     ml[2 * (((int64_t)g * H + h) * M + m) + 1] = l;
@@ -227,11 +239,12 @@ extern "C" int ifkv_prompt_attn_partial(int kv_dtype, const float* qd, const voi
 
 extern "C" int ifkv_prompt_attn_merge(const float* part_ml, const float* part_o, const int32_t* item_begin,
                                       int prompt_item0, int G, int H, int M, int Dh, float* ctx, float* ml,
-                                      void* stream) {
+                                      void* ctx_split3, void* stream) {
   IFKV_CHECK_ARG(Dh <= 256 && G > 0, "prompt_attn_merge: bad shape");
   int threads = ((Dh + 31) / 32) * 32;
-  prompt_attn_merge_kernel<<<G * H * M, threads, 0, as_stream(stream)>>>(part_ml, part_o, item_begin, prompt_item0,
-                                                                          H, M, Dh, ctx, ml);
+  prompt_attn_merge_kernel<<<G * H * M, threads, 0, as_stream(stream)>>>(
+      part_ml, part_o, item_begin, prompt_item0, H, M, Dh, ctx, ml, (__nv_bfloat16*)ctx_split3,
+      (int64_t)G * M * H * Dh);
   IFKV_LAUNCH_CHECK("prompt_attn_merge");
   return IFKV_OK;
 }

@@ -44,6 +44,26 @@ constexpr float kRescaleLog2 = 8.0f;
 #ifndef IFKV_ATTN_SETMAXNREG
 #define IFKV_ATTN_SETMAXNREG 0
 #endif
+// IFKV_ATTN_TRACE=1: CTA (0, 0) records globaltimer-free clock64 stamps of
+// every phase into a device buffer (tools/attn_trace.py reads it).
+#ifndef IFKV_ATTN_TRACE
+#define IFKV_ATTN_TRACE 0
+#endif
+#if IFKV_ATTN_TRACE
+__device__ long long g_attn_trace[12][4096];
+__device__ int g_attn_trace_n[12];
+#define TRACE(stream, val)                                                                          \
+  do {                                                                                              \
+    if (blockIdx.x == 0 && blockIdx.y == 0) {                                                       \
+      int i_ = g_attn_trace_n[stream]++;                                                            \
+      if (i_ < 4096) g_attn_trace[stream][i_] = (val);                                              \
+    }                                                                                               \
+  } while (0)
+#else
+#define TRACE(stream, val) \
+  do {                     \
+  } while (0)
+#endif
 #ifndef IFKV_ATTN_POLY_MASK
 #define IFKV_ATTN_POLY_MASK 0x00
 #endif
@@ -54,7 +74,7 @@ struct Smem {
   uint8_t v[2][kTile];
   uint64_t q_full;
   uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
-  uint64_t s_full[2], p_full[2], o_final[2];
+  uint64_t s_full[2], p_full[2][2], o_final[2];  // p_full[tile][key half]
   uint32_t tmem_base;
   int n_blocks[2];
 };
@@ -85,8 +105,17 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
   const uint32_t t_o = t_s + 128;
   float m_used = -INFINITY, l = 0.f;
   for (int j = 0; j < nblk; ++j) {
+    if (lane == 0 && w == 0) TRACE(x * 3 + 0, clock64());  // softmax: start waiting S
     tc::mbar_wait(&sm.s_full[x], j & 1);
     tc::tc_fence_after();
+    if (lane == 0 && w == 0) TRACE(x * 3 + 1, clock64());  // softmax: S ready
+#ifdef IFKV_ATTN_NOSOFTMAX  // experiment: pure MMA / TMA pipeline throughput
+    tc::tc_fence_before();
+    tc::mbar_arrive(&sm.p_full[x][0]);
+    tc::mbar_arrive(&sm.p_full[x][1]);
+    if (lane == 0 && w == 0) TRACE(x * 3 + 2, clock64());
+    continue;
+#endif
     const int j0 = j * kKeys;
     const bool masked = __any_sync(0xffffffffu, j0 + kKeys - 1 > hz);
     float v[64];
@@ -158,11 +187,14 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
       sum += sum2.x + sum2.y;
       tc::tmem_st16(t_s + hf * 32, pk);
       tc::tmem_st16(t_s + hf * 32 + 16, pk + 16);
+      // publish this half of P: the PV MMA over keys [64 hf, 64 hf + 64)
+      // starts while the next half is still being exponentiated
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&sm.p_full[x][hf]);
     }
     l = l * alpha + sum;
-    tc::tmem_st_wait();
-    tc::tc_fence_before();
-    tc::mbar_arrive(&sm.p_full[x]);
+    if (lane == 0 && w == 0) TRACE(x * 3 + 2, clock64());  // softmax: P published
   }
   // epilogue (a row that saw no key -- horizon -1 in partial mode -- writes 0)
   if (nblk > 0) {
@@ -230,7 +262,8 @@ __global__ void __launch_bounds__(384, 1)
       tc::mbar_init(&sm.v_full[i], 1);
       tc::mbar_init(&sm.v_empty[i], 1);
       tc::mbar_init(&sm.s_full[i], 1);
-      tc::mbar_init(&sm.p_full[i], 128);
+      tc::mbar_init(&sm.p_full[i][0], 128);
+      tc::mbar_init(&sm.p_full[i][1], 128);
       tc::mbar_init(&sm.o_final[i], 1);
     }
     tc::fence_barrier_init();
@@ -285,12 +318,19 @@ __global__ void __launch_bounds__(384, 1)
         }
         tc::mma_commit(&sm.s_full[x]);
       };
-      auto issue_pv = [&](int x, int j) {  // O_x += P_x(j) V_j, P from TMEM
+      auto issue_pv = [&](int x, int j) {  // O_x += P_x(j) V_j, P from TMEM, one key half at a time
         const uint32_t v_addr = tc::smem_u32(sm.v[j & 1]);
 #pragma unroll
-        for (int t = 0; t < kKeys / 16; ++t) {
-          uint64_t b = tc::smem_desc_sw128(v_addr + t * 2048, kPanel, 1024);
-          tc::mma_bf16_ts(tmem + 256 * x + 128, tmem + 256 * x + 8 * t, b, idesc_pv, (j > 0 || t > 0) ? 1u : 0u);
+        for (int hf = 0; hf < 2; ++hf) {
+          if (hf == 1) {
+            tc::mbar_wait(&sm.p_full[x][1], j & 1);
+            tc::tc_fence_after();
+          }
+#pragma unroll
+          for (int t = 4 * hf; t < 4 * hf + 4; ++t) {
+            uint64_t b = tc::smem_desc_sw128(v_addr + t * 2048, kPanel, 1024);
+            tc::mma_bf16_ts(tmem + 256 * x + 128, tmem + 256 * x + 8 * t, b, idesc_pv, (j > 0 || t > 0) ? 1u : 0u);
+          }
         }
         if (j == (x == 0 ? nA : nB) - 1) tc::mma_commit(&sm.o_final[x]);
       };
@@ -308,16 +348,22 @@ __global__ void __launch_bounds__(384, 1)
         for (int x = 0; x < 2; ++x) {
           const int nx = x == 0 ? nA : nB;
           if (j >= nx) continue;
-          tc::mbar_wait(&sm.p_full[x], j & 1);
+          TRACE(6, clock64());  // MMA: start waiting P_x
+          tc::mbar_wait(&sm.p_full[x][0], j & 1);
+          TRACE(7, clock64());  // MMA: P_x ready
           if (!v_ready) {
+            TRACE(8, clock64());  // MMA: start waiting V
             tc::mbar_wait(&sm.v_full[s], ph);
+            TRACE(9, clock64());
             v_ready = true;
           }
           tc::tc_fence_after();
           issue_pv(x, j);
           if (j + 1 < nx) {
             if (!next_k) {
+              TRACE(10, clock64());  // MMA: start waiting K
               tc::mbar_wait(&sm.k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+              TRACE(11, clock64());
               tc::tc_fence_after();
               next_k = true;
             }
@@ -386,4 +432,24 @@ extern "C" int ifkv_recompute_attn_tc(const void* q, const void* k_layer, const 
                                                                     (__nv_bfloat16*)out, ml_out);
   IFKV_LAUNCH_CHECK("recompute_attn_tc");
   return IFKV_OK;
+}
+
+// Debug: copy the phase trace of CTA (0, 0) out (IFKV_ATTN_TRACE builds only).
+extern "C" int ifkv_attn_trace_read(long long* out, int* counts, int reset) {
+#if IFKV_ATTN_TRACE
+  IFKV_CUDA_CALL(cudaDeviceSynchronize(), "trace");
+  IFKV_CUDA_CALL(cudaMemcpyFromSymbol(out, g_attn_trace, sizeof(g_attn_trace)), "trace");
+  IFKV_CUDA_CALL(cudaMemcpyFromSymbol(counts, g_attn_trace_n, sizeof(g_attn_trace_n)), "trace");
+  if (reset) {
+    int zero[12] = {0};
+    IFKV_CUDA_CALL(cudaMemcpyToSymbol(g_attn_trace_n, zero, sizeof(zero)), "trace");
+  }
+  return IFKV_OK;
+#else
+  (void)out;
+  (void)counts;
+  (void)reset;
+  ifkv::set_error("library built without IFKV_ATTN_TRACE");
+  return IFKV_ERR_ARG;
+#endif
 }

@@ -371,6 +371,7 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
     part_o = torch.empty((n_items, H, M, Dh), dtype=torch.float32, device=dev)
     ctx = torch.empty((G, M, H, Dh), dtype=torch.float32, device=dev)
     ml = torch.empty((G, H, M, 2), dtype=torch.float32, device=dev)
+    ctx3 = torch.empty((3, rows, d), dtype=torch.bfloat16, device=dev) if bf16 else None
     scale = 1.0 / math.sqrt(Dh)
     pending, pending_parts = None, 0
     last = cfg.n_layers - 1 if capture_layer is None else capture_layer
@@ -395,8 +396,9 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
                 N.call("ifkv_prompt_attn_partial", kv_dt, N.ptr(qd), N.ptr(slab_k[li]), N.ptr(slab_v[li]), N.ptr(kp),
                        N.ptr(vp), prompt_items_p, n_items - n_ctx, H, Hkv, M, Dh, scale,
                        part_ml.data_ptr() + n_ctx * stride_ml, part_o.data_ptr() + n_ctx * stride_o, _s())
+            fuse_split = bf16 and merge_hook is None and not capture
             N.call("ifkv_prompt_attn_merge", N.ptr(part_ml), N.ptr(part_o), ib_p, n_ctx if include_prompt else -1, G,
-                   H, M, Dh, N.ptr(ctx), N.ptr(ml), _s())
+                   H, M, Dh, N.ptr(ctx), N.ptr(ml), N.ptr(ctx3) if fuse_split else None, _s())
             if merge_hook is not None:
                 ctx_m, ml_m = merge_hook(ctx, ml)
                 ctx.copy_(ctx_m)
@@ -417,7 +419,10 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
                            Hkv, M, Dh, scale, N.ptr(scores), _s())
             out.scores, out.ml = scores, ml
             return out
-        cx = split3(ctx.view(rows, d)) if bf16 else ctx.view(rows, d)
+        if fuse_split:
+            cx = ctx3
+        else:
+            cx = split3(ctx.view(rows, d)) if bf16 else ctx.view(rows, d)
         o = mm_parts(cx, lw.wo)
         x2 = add_rmsnorm(h, o, o.shape[0], lw.mlp_norm, mode)
         gu = mm_parts(x2, lw.wgu)
