@@ -226,6 +226,7 @@ def run_ours(args, world, rank, local):
     E.PROFILE = None
     attn = prof.get("recompute_attn", [])
     attn_ms = [a.elapsed_time(b) for a, b, _ in attn]
+    sct = [(a.elapsed_time(b), w) for a, b, w in prof.get("qkv_rope_scatter", [])]
     rot = prof.get("rotate_rows", [])
     rot_ms = [a.elapsed_time(b) for a, b, _ in rot]
     del res
@@ -292,6 +293,14 @@ def run_ours(args, world, rank, local):
                     "unit": "GB/s", "frac": ach / PEAKS["hbm_gbs"], "avg_launch_ms": float(np.mean(rot_ms)),
                     "algorithmic_bytes_per_launch": rot_bytes}
 
+    sct_roof = None
+    if sct:  # fused rope + K/V scatter epilogue of the QKV GEMM (bytes per launch: qkv read, q/K/V written)
+        t_s, b_s = sum(t for t, _ in sct) / len(sct), sum(w for _, w in sct) / len(sct)
+        ach = b_s / (t_s / 1e3) / 1e9
+        sct_roof = {"kernel": "ifkv qkv_rope_scatter", "bound": "hbm", "achieved": ach, "peak": PEAKS["hbm_gbs"],
+                    "unit": "GB/s", "frac": ach / PEAKS["hbm_gbs"], "avg_launch_ms": t_s,
+                    "algorithmic_bytes_per_launch": b_s, "launches_per_step": len(sct)}
+
     # comparator: full bf16 prefill of the same context through the same kernels
     torch.cuda.synchronize()
     ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -325,6 +334,7 @@ def run_ours(args, world, rank, local):
         "ratio_vs_full_prefill": ms / full_ms,
         "roofline": roof,
         "roofline_kernel1": rot_roof,
+        "roofline_scatter": sct_roof,
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clk,

@@ -120,7 +120,7 @@ class AssembledCache:
 
     def token_ids_device(self):
         if self._token_ids_dev is None:
-            self._token_ids_dev = _torch().as_tensor(self.token_ids, device=self.keys.device)
+            self._token_ids_dev = E.h2d(self.token_ids, self.keys.device, np.int64)
         return self._token_ids_dev
 
     def in_decode_layout(self) -> bool:
@@ -231,15 +231,26 @@ def decode_targets(cache: AssembledCache) -> np.ndarray:
 def _delta_table(deltas: np.ndarray, d_head: int, rope_base: float, device):
     """Row table (int32, -1 for delta 0) and the fp64-derived cos/sin table
     of the distinct nonzero deltas."""
-    torch = _torch()
-    uniq, inv = np.unique(deltas, return_inverse=True)
-    tab = inv.astype(np.int32)
-    nz = uniq != 0
-    remap = np.full(uniq.size, -1, np.int32)
-    remap[nz] = np.arange(int(nz.sum()), dtype=np.int32)
-    tab = remap[tab]
-    cs = E.rope_table(uniq[nz] if nz.any() else np.zeros(1, np.int64), d_head, rope_base, device)
-    return torch.as_tensor(tab, device=device), cs
+    deltas = np.asarray(deltas, dtype=np.int64)
+    # runs of constant delta (one per chunk in the usual layouts): O(n), no sort
+    cut = np.flatnonzero(np.diff(deltas)) + 1
+    starts = np.concatenate([[0], cut])
+    run_d = deltas[starts]
+    if np.unique(run_d).size == run_d.size:  # every run has its own delta
+        nz = run_d != 0
+        rid = np.full(run_d.size, -1, np.int32)
+        rid[nz] = np.arange(int(nz.sum()), dtype=np.int32)
+        tab = np.repeat(rid, np.diff(np.concatenate([starts, [deltas.size]])))
+        uniq_nz = run_d[nz]
+    else:
+        uniq, inv = np.unique(deltas, return_inverse=True)
+        nzu = uniq != 0
+        remap = np.full(uniq.size, -1, np.int32)
+        remap[nzu] = np.arange(int(nzu.sum()), dtype=np.int32)
+        tab = remap[inv.astype(np.int32)]
+        uniq_nz = uniq[nzu]
+    cs = E.rope_table(uniq_nz if uniq_nz.size else np.zeros(1, np.int64), d_head, rope_base, device)
+    return E.h2d(tab.astype(np.int32), device), cs
 
 
 def decode_view(cache: AssembledCache, rope_base: float):

@@ -121,38 +121,64 @@ __global__ void __launch_bounds__(256) prompt_attn_partial_kernel(
   }
 }
 
-// grid (G * H * M), Dh threads (<= 256): merge the group's items in order.
+// grid (G * H * M), 256 threads = 8 warps: merge the group's items.
 // Items of group g: [item_begin[g], item_begin[g+1]) then, if
 // prompt_item0 >= 0, item prompt_item0 + g (the group's causal prompt item).
-// Two passes (max, then weighted sums) with 4 independent loads in flight.
-__global__ void prompt_attn_merge_kernel(const float* __restrict__ part_ml, const float* __restrict__ part_o,
-                                         const int32_t* __restrict__ item_begin, int prompt_item0, int H, int M,
-                                         int Dh, float* __restrict__ ctx, float* __restrict__ ml,
-                                         __nv_bfloat16* __restrict__ ctx3, int64_t plane) {
+// Warp w takes items k = w, w + 8, ...; lane owns Dh/32 (<= 4) consecutive
+// dims as one vector load.  Warp partials combine in warp order through smem
+// (fixed order -> deterministic).
+__global__ void __launch_bounds__(256) prompt_attn_merge_kernel(
+    const float* __restrict__ part_ml, const float* __restrict__ part_o, const int32_t* __restrict__ item_begin,
+    int prompt_item0, int H, int M, int Dh, float* __restrict__ ctx, float* __restrict__ ml,
+    __nv_bfloat16* __restrict__ ctx3, int64_t plane) {
+  __shared__ float s_m[8], s_l[8];
+  __shared__ float s_o[8][256];
   const int r = blockIdx.x;  // (g, h, m)
   const int m = r % M, h = (r / M) % H, g = r / (M * H);
   const int b = item_begin[g], e = item_begin[g + 1];
   const int n = e - b + (prompt_item0 >= 0 ? 1 : 0);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int per = (Dh + 31) / 32;  // dims per lane (<= 8)
   auto row_of = [&](int k) -> int64_t {
     const int it = k < e - b ? b + k : prompt_item0 + g;
     return ((int64_t)it * H + h) * M + m;
   };
+  // pass 1: max over all items (every warp computes it redundantly -> no sync)
   float mx = -INFINITY;
-#pragma unroll 4
-  for (int k = 0; k < n; ++k) mx = fmaxf(mx, part_ml[2 * row_of(k)]);
-  float l = 0.f, o = 0.f;
-  const int d = threadIdx.x;
-#pragma unroll 4
-  for (int k = 0; k < n; ++k) {
+  for (int k = lane; k < n; k += 32) mx = fmaxf(mx, part_ml[2 * row_of(k)]);
+  mx = warp_max(mx);
+  // pass 2: this warp's items, weighted
+  float l = 0.f, o[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) o[u] = 0.f;
+  const int d0 = lane * per;
+  for (int k = w; k < n; k += 8) {
     const int64_t row = row_of(k);
     const float mi = part_ml[2 * row];
     const float a = mi == -INFINITY ? 0.f : expf(mi - mx);
     l += part_ml[2 * row + 1] * a;
-    if (d < Dh) o += part_o[row * Dh + d] * a;
+    const float* src = part_o + row * Dh + d0;
+    if (per == 4 && d0 < Dh) {
+      const float4 v = *reinterpret_cast<const float4*>(src);
+      o[0] += v.x * a; o[1] += v.y * a; o[2] += v.z * a; o[3] += v.w * a;
+    } else {
+      for (int u = 0; u < per; ++u)
+        if (d0 + u < Dh) o[u] += src[u] * a;
+    }
   }
-  const float c = l > 0.f ? o / l : 0.f;  // no item: empty shard
-  const int64_t ci = (((int64_t)g * M + m) * H + h) * Dh + d;
-  if (d < Dh) {
+  if (lane == 0) s_l[w] = l;
+  for (int u = 0; u < per; ++u)
+    if (d0 + u < Dh) s_o[w][d0 + u] = o[u];
+  __syncthreads();
+  float lt = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) lt += s_l[k];
+  for (int d = threadIdx.x; d < Dh; d += blockDim.x) {
+    float ot = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ot += s_o[k][d];
+    const float c = lt > 0.f ? ot / lt : 0.f;  // no item: empty shard
+    const int64_t ci = (((int64_t)g * M + m) * H + h) * Dh + d;
     ctx[ci] = c;
     if (ctx3) {  // fused hi/mid/lo split of the next GEMM's operand
       __nv_bfloat16 a0, a1, a2;
@@ -162,10 +188,11 @@ __global__ void prompt_attn_merge_kernel(const float* __restrict__ part_ml, cons
       ctx3[2 * plane + ci] = a2;
     }
   }
-  if (d == 0) {
+  if (threadIdx.x == 0) {
     ml[2 * (((int64_t)g * H + h) * M + m)] = mx;
-    ml[2 * (((int64_t)g * H + h) * M + m) + 1] = l;
+    ml[2 * (((int64_t)g * H + h) * M + m) + 1] = lt;
   }
+  (void)s_m;
 }
 
 // grid (n_items), 128 threads: thread j owns key column j of the item and
@@ -241,8 +268,7 @@ extern "C" int ifkv_prompt_attn_merge(const float* part_ml, const float* part_o,
                                       int prompt_item0, int G, int H, int M, int Dh, float* ctx, float* ml,
                                       void* ctx_split3, void* stream) {
   IFKV_CHECK_ARG(Dh <= 256 && G > 0, "prompt_attn_merge: bad shape");
-  int threads = ((Dh + 31) / 32) * 32;
-  prompt_attn_merge_kernel<<<G * H * M, threads, 0, as_stream(stream)>>>(
+  prompt_attn_merge_kernel<<<G * H * M, 256, 0, as_stream(stream)>>>(
       part_ml, part_o, item_begin, prompt_item0, H, M, Dh, ctx, ml, (__nv_bfloat16*)ctx_split3,
       (int64_t)G * M * H * Dh);
   IFKV_LAUNCH_CHECK("prompt_attn_merge");

@@ -231,10 +231,65 @@ __device__ __forceinline__ void store8(__nv_bfloat16* d, const float* x) {
   *reinterpret_cast<uint4*>(d) = v;
 }
 
-// Vectorised variant (Dh % 8 == 0): one thread = 8 consecutive elements
-// (4 pairs) of one head row.
+// Vectorised variant (Dh % 8 == 0): one CTA per row (no index division);
+// thread = 8 consecutive elements (4 pairs) of one head row, up to kU such
+// vectors per thread with all loads issued before any store.
+template <typename TIn, typename TOut, int kU>
+__global__ void __launch_bounds__(256) qkv_rope_scatter_vec_kernel(
+    const TIn* __restrict__ qkv, int n_parts, int64_t part_stride, int rows, int H, int Hkv, int Dh,
+    const float2* __restrict__ cs, TOut* __restrict__ q_out, TOut* __restrict__ k_dst, TOut* __restrict__ v_dst,
+    const int64_t* __restrict__ dst_rows) {
+  const int half = Dh / 2;
+  const int vpr = (H + 2 * Hkv) * Dh / 8;  // vectors per row
+  const int r = blockIdx.x;
+  const int64_t drow = dst_rows ? dst_rows[r] : r;
+  const TIn* src = qkv + (int64_t)r * (H + 2 * Hkv) * Dh;
+  const float2* csr = cs + (int64_t)r * half;
+  const int q_end = q_out ? 0 : H * Dh / 8;  // vectors below q_end are skipped (no q output)
+  for (int v0 = q_end + threadIdx.x; v0 < vpr; v0 += kU * blockDim.x) {
+    float x[kU][8];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int v = v0 + u * blockDim.x;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) x[u][e] = 0.f;
+      if (v < vpr)
+        for (int p = 0; p < n_parts; ++p) load8_add(src + p * part_stride + v * 8, x[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int v = v0 + u * blockDim.x;
+      if (v >= vpr) break;
+      const int c8 = v * 8, head = c8 / Dh, e0 = c8 - head * Dh;
+      if (head < H + Hkv) {
+        const float4* c4 = reinterpret_cast<const float4*>(csr + e0 / 2);
+        const float4 ab = __ldg(c4), cd = __ldg(c4 + 1);
+        const float2 a[4] = {make_float2(ab.x, ab.y), make_float2(ab.z, ab.w), make_float2(cd.x, cd.y),
+                             make_float2(cd.z, cd.w)};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float y0 = x[u][2 * q] * a[q].x - x[u][2 * q + 1] * a[q].y;
+          const float y1 = x[u][2 * q] * a[q].y + x[u][2 * q + 1] * a[q].x;
+          x[u][2 * q] = y0;
+          x[u][2 * q + 1] = y1;
+        }
+      }
+      TOut* d;
+      if (head < H)
+        d = q_out + ((int64_t)r * H + head) * Dh + e0;
+      else if (head < H + Hkv)
+        d = k_dst + (drow * Hkv + (head - H)) * Dh + e0;
+      else
+        d = v_dst + (drow * Hkv + (head - H - Hkv)) * Dh + e0;
+      store8(d, x[u]);
+    }
+  }
+}
+
+// Grid-stride variant (A/B, IFKV_SCATTER_ROW=0): one thread = 8 consecutive
+// elements (4 pairs) of one head row per iteration.
 template <typename TIn, typename TOut>
-__global__ void qkv_rope_scatter_vec_kernel(const TIn* __restrict__ qkv, int n_parts, int64_t part_stride, int rows,
+__global__ void qkv_rope_scatter_strided_kernel(const TIn* __restrict__ qkv, int n_parts, int64_t part_stride, int rows,
                                             int H, int Hkv, int Dh, const float2* __restrict__ cs,
                                             TOut* __restrict__ q_out, TOut* __restrict__ k_dst,
                                             TOut* __restrict__ v_dst, const int64_t* __restrict__ dst_rows) {
@@ -373,18 +428,28 @@ extern "C" int ifkv_qkv_rope_scatter(const void* qkv, int qkv_dtype, int n_parts
   unsigned grid = (unsigned)((total + 255) / 256);
   auto c = reinterpret_cast<const float2*>(cs);
   cudaStream_t s = as_stream(stream);
-  const bool vec = Dh % 8 == 0;
-  if (vec) {
+#ifndef IFKV_SCATTER_ROW
+#define IFKV_SCATTER_ROW 1
+#endif
+  const bool row_kernel = IFKV_SCATTER_ROW && Dh % 8 == 0 && (H + 2 * Hkv) * Dh / 8 <= 4 * 256;
+  const bool strided = !row_kernel && Dh % 8 == 0;
+  if (row_kernel) {
+    grid = (unsigned)rows;
+  } else if (strided) {
     int64_t nv = (int64_t)rows * (H + 2 * Hkv) * Dh / 8;
     int64_t want = (nv + 255) / 256;
     grid = (unsigned)(want < 148 * 16 ? want : 148 * 16);
   }
-#define IFKV_QKV_LAUNCH(TI, TO)                                                                                   \
-  if (vec)                                                                                                        \
-    qkv_rope_scatter_vec_kernel<TI, TO><<<grid, 256, 0, s>>>((const TI*)qkv, n_parts, part_stride, rows, H, Hkv,   \
-                                                             Dh, c, (TO*)q_out, (TO*)k_dst, (TO*)v_dst, dst_rows); \
-  else                                                                                                            \
-    qkv_rope_scatter_kernel<TI, TO><<<grid, 256, 0, s>>>((const TI*)qkv, n_parts, part_stride, rows, H, Hkv, Dh, c, \
+#define IFKV_QKV_LAUNCH(TI, TO)                                                                                     \
+  if (row_kernel)                                                                                                   \
+    qkv_rope_scatter_vec_kernel<TI, TO, 4><<<grid, 256, 0, s>>>((const TI*)qkv, n_parts, part_stride, rows, H, Hkv, \
+                                                                Dh, c, (TO*)q_out, (TO*)k_dst, (TO*)v_dst, dst_rows); \
+  else if (strided)                                                                                                 \
+    qkv_rope_scatter_strided_kernel<TI, TO><<<grid, 256, 0, s>>>((const TI*)qkv, n_parts, part_stride, rows, H, Hkv, \
+                                                                 Dh, c, (TO*)q_out, (TO*)k_dst, (TO*)v_dst,        \
+                                                                 dst_rows);                                        \
+  else                                                                                                              \
+    qkv_rope_scatter_kernel<TI, TO><<<grid, 256, 0, s>>>((const TI*)qkv, n_parts, part_stride, rows, H, Hkv, Dh, c,  \
                                                          (TO*)q_out, (TO*)k_dst, (TO*)v_dst, dst_rows)
   if (qkv_dtype == IFKV_F32 && out_dtype == IFKV_F32) IFKV_QKV_LAUNCH(float, float);
   else if (qkv_dtype == IFKV_F32) IFKV_QKV_LAUNCH(float, __nv_bfloat16);

@@ -195,19 +195,26 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_as_u64(a)), "l"(f2_as_u64(b)));
   return u64_as_f2(d);
 }
-// ex2_poly on a pair with packed arithmetic (same polynomial, same exactness
-// for masked inputs).
+// ex2_poly on a pair with packed arithmetic: 2 FMNMX + 3 FADD2 + 3 FFMA2 +
+// 4 integer ops for two exponentials, no MUFU.  Inputs below -126 (masked
+// -inf included) give 2^-126 * p ~ 1e-38 instead of 0: below every bf16 P
+// that matters (the row sum is >= 1) and exactly representable.
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_as_u64(a)), "l"(f2_as_u64(b)));
+  return u64_as_f2(d);
+}
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   const float2 xc = make_float2(fmaxf(x.x, -126.f), fmaxf(x.y, -126.f));
-  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23: low mantissa bits = round(x)
   const float2 t = fadd2(xc, magic);
-  const float2 f = fadd2(xc, fadd2(magic, make_float2(-t.x, -t.y)));
+  const float2 f = fsub2(xc, fsub2(t, magic));  // f in [-1/2, 1/2]
   float2 p = ffma2(make_float2(0.05295114f, 0.05295114f), f, make_float2(0.24165066f, 0.24165066f));
   p = ffma2(p, f, make_float2(0.69353656f, 0.69353656f));
   p = ffma2(p, f, make_float2(1.f, 1.f));
-  const float r0 = __int_as_float(__float_as_int(t.x) * 8388608 + __float_as_int(p.x));
-  const float r1 = __int_as_float(__float_as_int(t.y) * 8388608 + __float_as_int(p.y));
-  return make_float2(x.x < -126.f ? 0.f : r0, x.y < -126.f ? 0.f : r1);
+  // bits(t) << 23 == round(x) << 23 (the magic's own bits shift out)
+  return make_float2(__int_as_float((__float_as_int(t.x) << 23) + __float_as_int(p.x)),
+                     __int_as_float((__float_as_int(t.y) << 23) + __float_as_int(p.y)));
 }
 
 __device__ __forceinline__ float max3(float a, float b, float c) {
@@ -219,6 +226,19 @@ __device__ __forceinline__ float max3(float a, float b, float c) {
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// (a, b) = hi + mid + lo as three packed bf16 pairs (same terms as split3):
+// 3 F2FP + 4 integer unpacks + 2 FADD2 per pair.
+__device__ __forceinline__ float2 unpack_bf16(uint32_t u) {
+  return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
+}
+__device__ __forceinline__ void split3_pair(float a, float b, uint32_t& hi, uint32_t& mid, uint32_t& lo) {
+  hi = pack_bf16(a, b);
+  float2 r = fsub2(make_float2(a, b), unpack_bf16(hi));
+  mid = pack_bf16(r.x, r.y);
+  r = fsub2(r, unpack_bf16(mid));
+  lo = pack_bf16(r.x, r.y);
 }
 
 }  // namespace tc

@@ -159,10 +159,12 @@ __global__ void __launch_bounds__(192, 1)
     const int h = h0 + (valid ? row / M : 0);
     const int m = valid ? row % M : 0;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
-    float m_used = -INFINITY, l = 0.f, mf = 0.f, inv_lf = 0.f;
+    // m_used: running max of the RAW scores; exponentials in log2 units
+    const float sl2 = scale * 1.4426950408889634f;
+    float m_used = -INFINITY, l = 0.f, mf2 = 0.f, inv_lf = 0.f;
     if (mode == 1 && valid) {
       const int64_t s = 2 * (((int64_t)it.group * H + h) * M + m);
-      mf = ml_final[s];
+      mf2 = ml_final[s] * 1.4426950408889634f;  // natural-unit max of the scaled logits -> log2 units
       inv_lf = 1.f / ml_final[s + 1];
     }
     float* T = reinterpret_cast<float*>(sm.v[0]);  // mode 1 transpose, [key][row ^ (key & 31)]
@@ -176,25 +178,41 @@ __global__ void __launch_bounds__(192, 1)
       tc::tmem_ld_wait();
       tc::tc_fence_before();
       tc::mbar_arrive(&sm.s_free);  // S may be overwritten by S(j+1) from here on
+      if (nk < 128) {  // last block of a run only
 #pragma unroll
-      for (int c = 0; c < 128; ++c) v[c] = c < nk ? v[c] * scale : -INFINITY;
+        for (int c = 0; c < 128; ++c)
+          if (c >= nk) v[c] = -INFINITY;
+      }
       if (mode == 0) {
-        float mx = -INFINITY;
+        // raw-score max (scale > 0 commutes with max), four FMNMX3 chains
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-        for (int c = 0; c < 128; c += 2) mx = tc::max3(mx, v[c], v[c + 1]);
+        for (int c = 0; c < 128; c += 8) {
+          m4[0] = tc::max3(m4[0], v[c], v[c + 1]);
+          m4[1] = tc::max3(m4[1], v[c + 2], v[c + 3]);
+          m4[2] = tc::max3(m4[2], v[c + 4], v[c + 5]);
+          m4[3] = tc::max3(m4[3], v[c + 6], v[c + 7]);
+        }
+        const float mx = tc::max3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
         float alpha = 1.f;
         bool need = false;
-        if (m_used == -INFINITY || mx - m_used > kRescale) {
+        if (m_used == -INFINITY || (mx - m_used) * scale > kRescale) {
           need = true;
-          alpha = m_used == -INFINITY ? 0.f : expf(m_used - mx);
+          alpha = m_used == -INFINITY ? 0.f : tc::ex2((m_used - mx) * sl2);
           m_used = mx;
         }
-        float sum = 0.f;
+        // p = 2^(s sl2 - m sl2): packed FFMA2 + MUFU ex2 (fp32 accurate to ~2 ulp)
+        const float2 sc2 = make_float2(sl2, sl2), mb2 = make_float2(-m_used * sl2, -m_used * sl2);
+        float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-        for (int c = 0; c < 128; ++c) {
-          v[c] = expf(v[c] - m_used);
-          sum += v[c];
+        for (int c = 0; c < 128; c += 2) {
+          const float2 x = tc::ffma2(make_float2(v[c], v[c + 1]), sc2, mb2);
+          const float2 e = make_float2(tc::ex2(x.x), tc::ex2(x.y));
+          v[c] = e.x;
+          v[c + 1] = e.y;
+          sum2[(c >> 1) & 1] = tc::fadd2(sum2[(c >> 1) & 1], e);
         }
+        const float sum = (sum2[0].x + sum2[1].x) + (sum2[0].y + sum2[1].y);
         // P(j-1) consumed and O = PV(0..j-1) complete
         if (j > 0) tc::mbar_wait(&sm.pv_done, (j - 1) & 1);
         tc::tc_fence_after();
@@ -215,18 +233,7 @@ __global__ void __launch_bounds__(192, 1)
         for (int q = 0; q < 4; ++q) {
           uint32_t p0[16], p1[16], p2[16];
 #pragma unroll
-          for (int u = 0; u < 16; ++u) {
-            __nv_bfloat16 a0, a1, a2, b0, b1, b2;
-            split3(v[32 * q + 2 * u], a0, a1, a2);
-            split3(v[32 * q + 2 * u + 1], b0, b1, b2);
-            __nv_bfloat162 x0, x1, x2;
-            x0.x = a0; x0.y = b0;
-            x1.x = a1; x1.y = b1;
-            x2.x = a2; x2.y = b2;
-            p0[u] = *reinterpret_cast<uint32_t*>(&x0);
-            p1[u] = *reinterpret_cast<uint32_t*>(&x1);
-            p2[u] = *reinterpret_cast<uint32_t*>(&x2);
-          }
+          for (int u = 0; u < 16; ++u) tc::split3_pair(v[32 * q + 2 * u], v[32 * q + 2 * u + 1], p0[u], p1[u], p2[u]);
           tc::tmem_st16(tmem + lane_off + kColP + 0 * 64 + 16 * q, p0);
           tc::tmem_st16(tmem + lane_off + kColP + 1 * 64 + 16 * q, p1);
           tc::tmem_st16(tmem + lane_off + kColP + 2 * 64 + 16 * q, p2);
@@ -239,7 +246,8 @@ __global__ void __launch_bounds__(192, 1)
         // p = exp(s - m_final) / l_final -> transposed smem -> column sums
         asm volatile("bar.sync 1, 128;" ::: "memory");  // previous block's column reads done
 #pragma unroll
-        for (int c = 0; c < 128; ++c) T[c * 128 + (row ^ (c & 31))] = valid ? expf(v[c] - mf) * inv_lf : 0.f;
+        for (int c = 0; c < 128; ++c)
+          T[c * 128 + (row ^ (c & 31))] = valid ? tc::ex2(fmaf(v[c], sl2, -mf2)) * inv_lf : 0.f;
         asm volatile("bar.sync 1, 128;" ::: "memory");
         const int c = row;  // this thread sums key column c over the tile rows
         float acc = 0.f;
@@ -265,7 +273,7 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
       if (valid) {
-        part_ml[2 * row_id] = m_used;
+        part_ml[2 * row_id] = m_used * scale;  // natural units of the scaled logits
         part_ml[2 * row_id + 1] = l;
       }
     }

@@ -173,10 +173,11 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
 #pragma unroll
       for (int c = 0; c < 64; c += 2) {
         // packed x = s * scale - m; exp2 on the MUFU, or on the FMA pipe for
-        // the pairs selected by IFKV_ATTN_POLY_MASK (ex2.approx.ftz(-inf) = +0)
+        // the pairs selected by IFKV_ATTN_POLY_MASK in unmasked blocks
+        // (ex2.approx.ftz(-inf) = +0 on the masked ones)
         const float2 xx = tc::ffma2(make_float2(v[c], v[c + 1]), sc2, mb2);
         float2 e;
-        if ((IFKV_ATTN_POLY_MASK >> ((c >> 1) & 7)) & 1) {
+        if (!masked && ((IFKV_ATTN_POLY_MASK >> ((c >> 1) & 7)) & 1)) {  // masked blocks keep exact zeros
           e = tc::ex2_poly2(xx);
         } else {
           e = make_float2(tc::ex2(xx.x), tc::ex2(xx.y));

@@ -19,6 +19,7 @@ sm_100a kernel behind include/ifkv.h.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence, Tuple
 
@@ -81,11 +82,23 @@ def require_cuda(t, what: str):
 # ---------------------------------------------------------------------------
 
 
+def h2d(a, device, dtype=None):
+    """Host array -> device tensor through a pinned staging buffer with a
+    non-blocking copy: the host never waits on the stream (pageable copies
+    can), so it keeps running ahead of the GPU.  The caching host allocator
+    does not reuse the staging buffer before the copy has completed."""
+    torch = _torch()
+    arr = np.ascontiguousarray(a if dtype is None else np.asarray(a, dtype=dtype))
+    if arr.size == 0:
+        return torch.from_numpy(arr).to(device)
+    return torch.from_numpy(arr).pin_memory().to(device, non_blocking=True)
+
+
 def to_device_i64(a, device):
     torch = _torch()
     if isinstance(a, torch.Tensor):
         return a.to(device=device, dtype=torch.int64)
-    return torch.as_tensor(np.asarray(a, dtype=np.int64), device=device)
+    return h2d(a, device, np.int64)
 
 
 def rope_table(positions, d_head: int, base: float, device) -> "object":
@@ -190,7 +203,7 @@ def topk_segments(scores, seg_begin, seg_k, agg_mode: int = N.AGG_NONE):
     seg_begin = np.asarray(seg_begin, dtype=np.int32)
     seg_k = np.asarray(seg_k, dtype=np.int32)
     out_begin = np.concatenate([[0], np.cumsum(seg_k)]).astype(np.int32)
-    meta = torch.as_tensor(np.concatenate([seg_begin, seg_k, out_begin]), device=dev)
+    meta = h2d(np.concatenate([seg_begin, seg_k, out_begin]), dev)
     nseg = seg_k.size
     out = torch.empty(int(out_begin[-1]), dtype=torch.int64, device=dev)
     agg = torch.empty(nseg, dtype=torch.float64, device=dev) if agg_mode != N.AGG_NONE else None
@@ -238,6 +251,28 @@ def mm_parts(x, w):
         y = torch.mm(x.reshape(p * rows, k), w, out_dtype=torch.float32)
         return y.view(p, rows, w.shape[1])
     return torch.mm(x, w).unsqueeze(0)
+
+
+# Residual adds of the layer stack inside the O-proj / down-proj GEMMs
+# (cuBLAS epilogue with the fp32 residual stream as C, beta = 1) instead of
+# an fp32 GEMM output re-read by add_rmsnorm.  IFKV_FUSED_RESIDUAL=0 restores
+# the separate add (A/B).
+FUSED_RESIDUAL = os.environ.get("IFKV_FUSED_RESIDUAL", "1") != "0"
+
+
+def mm_f32(a, w):
+    """a @ w with an fp32 result (bf16 operands accumulate in fp32)."""
+    torch = _torch()
+    return torch.mm(a, w, out_dtype=torch.float32) if a.dtype != torch.float32 else torch.mm(a, w)
+
+
+def residual_mm(h, a, w):
+    """h += a @ w in place, fp32 h, fp32 accumulation."""
+    torch = _torch()
+    if a.dtype == torch.float32:
+        h.addmm_(a, w)
+    else:
+        torch.addmm(h, a, w, out_dtype=torch.float32, out=h)
 
 
 # ---------------------------------------------------------------------------
@@ -345,14 +380,14 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
     item_keys = _tc_item_keys(groups, Hkv, H // Hkv, M) if use_tc else ITEM_KEYS
     items_np, ctx_begin_np, n_ctx, qg_np, qc_np, deltas = _plan_items(groups, M, item_keys)
     n_items, n_qsets = items_np.shape[0], qg_np.size
-    meta = torch.as_tensor(np.concatenate([items_np.ravel(), ctx_begin_np, qg_np, qc_np]), device=dev)
+    meta = h2d(np.concatenate([items_np.ravel(), ctx_begin_np, qg_np, qc_np]), dev)
     items_p = meta.data_ptr()
     prompt_items_p = items_p + 24 * n_ctx
     ib_p = items_p + 4 * items_np.size
     qg_p = ib_p + 4 * ctx_begin_np.size
     qc_p = qg_p + 4 * qg_np.size
     cs_delta = rope_table(np.asarray(deltas, np.int64) if deltas else np.zeros(1, np.int64), Dh, cfg.rope_base, dev)
-    ids = torch.as_tensor(np.concatenate([np.asarray(g.token_ids, np.int64) for g in groups]), device=dev)
+    ids = h2d(np.concatenate([np.asarray(g.token_ids, np.int64) for g in groups]), dev)
     pos_all = np.concatenate([np.asarray(g.positions, np.int64) for g in groups])
     if pos_all.min() < 0 or pos_all.max() >= cfg.max_position:
         raise ConfigurationError(f"position outside [0, {cfg.max_position}): {int(pos_all.max())}")
@@ -468,7 +503,10 @@ def layer_stack(weights, token_ids, positions, k_slab, v_slab, dst_rows, horizon
         final = li == cfg.n_layers - 1 and not want_hidden
         x = add_rmsnorm(h, pending, 1, lw.attn_norm, act_mode)
         qkv = torch.mm(x, lw.wqkv)
-        qkv_rope_scatter(qkv, 1, H, Hkv, Dh, cs, None if final else qbuf, k_slab[li], v_slab[li], dst_rows)
+        esz = qkv.element_size()
+        moved = S * ((2 * Hkv * Dh) * 2 + (0 if final else 2 * H * Dh)) * esz  # read + write (q skipped when final)
+        with _Bracket("qkv_rope_scatter", moved):
+            qkv_rope_scatter(qkv, 1, H, Hkv, Dh, cs, None if final else qbuf, k_slab[li], v_slab[li], dst_rows)
         if final:
             return None
         if attn_fn is not None:  # chunk-sharded: attention over every rank's keys
@@ -476,11 +514,17 @@ def layer_stack(weights, token_ids, positions, k_slab, v_slab, dst_rows, horizon
         else:
             with _Bracket("recompute_attn", li):
                 recompute_attn(qbuf, k_slab[li], v_slab[li], horizon, H, Hkv, Dh, out=attn_out)
-        o = torch.mm(attn_out.view(S, d), lw.wo, out_dtype=torch.float32) if bf16 else torch.mm(attn_out.view(S, d),
-                                                                                                 lw.wo)
-        x2 = add_rmsnorm(h, o, 1, lw.mlp_norm, act_mode)
+        if FUSED_RESIDUAL:  # h += attn Wo inside the GEMM (fp32 C operand, beta = 1)
+            residual_mm(h, attn_out.view(S, d), lw.wo)
+            x2 = add_rmsnorm(h, None, 0, lw.mlp_norm, act_mode)
+        else:
+            x2 = add_rmsnorm(h, mm_f32(attn_out.view(S, d), lw.wo), 1, lw.mlp_norm, act_mode)
         gu = torch.mm(x2, lw.wgu)
         a = silu_mul(gu, 1, cfg.d_ff, act_mode)
-        pending = torch.mm(a, lw.wdown, out_dtype=torch.float32) if bf16 else torch.mm(a, lw.wdown)
-    residual_add(h, pending, 1)
+        if FUSED_RESIDUAL:
+            residual_mm(h, a, lw.wdown)
+        else:
+            pending = mm_f32(a, lw.wdown)
+    if pending is not None:
+        residual_add(h, pending, 1)
     return h

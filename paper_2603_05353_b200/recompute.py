@@ -109,13 +109,20 @@ def recompute_selected(weights, cache: AssembledCache, plan: RecomputePlan) -> A
     sel = E.to_device_i64(plan.selected, dev)
     pos = E.to_device_i64(plan.positions, dev)
     upto = E.to_device_i64(plan.allowed_upto, dev)
+    readback = None
+    if plan.trusted:  # device plan: start its copy to the host now, read it after the layer stack is queued
+        readback = [torch.empty(t.shape, dtype=torch.int64, pin_memory=True) for t in (sel, pos)]
+        for h, t in zip(readback, (sel, pos)):
+            h.copy_(t, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record()
     to_decode_layout(cache, cfg.rope_base)
     ids = cache.token_ids_device().index_select(0, sel)
     E.layer_stack(weights, ids, pos, cache.keys, cache.values, sel, upto)
     # row metadata (host): positions and provenance of the replaced rows
-    if plan.trusted:
-        sel_h = plan.selected.cpu().numpy()
-        pos_h = sel_h if plan.positions is plan.selected else plan.positions.cpu().numpy()
+    if readback is not None:
+        done.synchronize()  # waits for the selection only, not for the recompute
+        sel_h, pos_h = readback[0].numpy(), readback[1].numpy()
     else:
         sel_h, pos_h = plan.selected, plan.positions
     cache.row_positions[sel_h] = pos_h

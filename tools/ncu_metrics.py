@@ -1,0 +1,24 @@
+"""Print key metrics of ncu reports: python tools/ncu_metrics.py a.ncu-rep [...]"""
+import csv
+import io
+import subprocess
+import sys
+
+WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
+        "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+        "lts__t_sector_hit_rate.pct", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__cycles_elapsed.avg.per_second"]
+
+for f in sys.argv[1:]:
+    out = subprocess.run(["ncu", "-i", f, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h, u = rows[0], rows[1]
+    print(f"== {f}")
+    for r in rows[2:]:
+        print("  kernel:", r[h.index("Kernel Name")][:90])
+        for w in WANT:
+            if w in h:
+                i = h.index(w)
+                print(f"    {w} = {r[i]} {u[i]}")
