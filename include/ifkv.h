@@ -93,6 +93,10 @@ int ifkv_silu_mul(const void* gu, int gu_dtype, int n_parts, int rows, int d_ff,
 int ifkv_embed_rows(const void* table, int dtype, const int64_t* ids, int rows, int d, float* h, void* stream);
 /* out = sum over n_parts of x (fp32 blocks of n elements) -> fp32 or split3. */
 int ifkv_split3(const float* x, int64_t n, void* out, void* stream);
+/* acc[r] += || a[r] - b[r] ||_2 for fp32 [rows][d] (fp64 accumulator): the
+ * CacheBlend baseline's per-token hidden-state deviation
+ * (replaces np.linalg.norm in selection.py:219-222). */
+int ifkv_row_dist_accum(const float* a, const float* b, int rows, int d, double* acc, void* stream);
 
 /* ---- fresh q/k/v (model.py:433-437, recompute.py:99-112) ----------------
  * qkv = [rows][(H + 2 Hkv) Dh] (GEMM output, qkv_dtype, n_parts part blocks

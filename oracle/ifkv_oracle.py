@@ -508,6 +508,26 @@ def select_topk(scores, k: int) -> np.ndarray:
     return np.sort(order[:k]).astype(np.int64)
 
 
+def score_cacheblend(weights, chunk_token_ids: Sequence, early_layers: int) -> np.ndarray:
+    """CacheBlend baseline (selection.py:190-223): per token, the Euclidean
+    distance between its block outputs in the chunk-local runs (positions
+    0..len-1, causal within the chunk) and in one full-context causal run,
+    summed over the first ``early_layers`` layers."""
+    cfg = weights.config
+    if early_layers < 1 or early_layers > cfg.n_layers:
+        raise OracleError(f"early_layers {early_layers} outside [1, {cfg.n_layers}]")
+    if not len(chunk_token_ids):
+        raise OracleError("no chunks to score")
+    local = [decoder_forward(weights, t, np.arange(len(t)), want_logits=False).hidden for t in chunk_token_ids]
+    full_tok = np.concatenate([np.asarray(t, np.int64) for t in chunk_token_ids])
+    full = decoder_forward(weights, full_tok, np.arange(full_tok.size), want_logits=False).hidden
+    scores = np.zeros(full_tok.size, np.float64)
+    for li in range(early_layers):
+        loc = np.concatenate([h[li] for h in local], axis=0)
+        scores += np.linalg.norm(loc - full[li], axis=1)
+    return scores
+
+
 def run_selection(weights, cache: Assembled, prompt_ids, ratio=None, topk=None, mode="GLOBAL",
                   norm_layer=None, prompt_offset=None):
     """Attention-norm strategy dispatch (selection.py:263-300).

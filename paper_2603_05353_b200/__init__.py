@@ -46,6 +46,7 @@ from .selection import (
     default_norm_layer,
     run_selection,
     score_attention_norm,
+    score_cacheblend,
     score_from_attention,
     select_epic,
     select_random,

@@ -185,9 +185,45 @@ __global__ void split3_kernel(const float* __restrict__ x, int64_t n, __nv_bfloa
   out[2 * n + t] = c;
 }
 
+// One warp per row: acc[r] += sqrt(sum_c (a - b)^2), fp32 lane partials,
+// fp64 cross-lane sum (CacheBlend hidden-state deviation, selection.py:219-222).
+__global__ void __launch_bounds__(256) row_dist_accum_kernel(const float* __restrict__ a, const float* __restrict__ b,
+                                                             int rows, int d, double* __restrict__ acc) {
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float* pa = a + (int64_t)r * d;
+  const float* pb = b + (int64_t)r * d;
+  float s = 0.f;
+  if (d % 4 == 0) {
+    for (int c = lane * 4; c < d; c += 128) {
+      const float4 x = *reinterpret_cast<const float4*>(pa + c), y = *reinterpret_cast<const float4*>(pb + c);
+      const float e0 = x.x - y.x, e1 = x.y - y.y, e2 = x.z - y.z, e3 = x.w - y.w;
+      s += (e0 * e0 + e1 * e1) + (e2 * e2 + e3 * e3);
+    }
+  } else {
+    for (int c = lane; c < d; c += 32) {
+      const float e = pa[c] - pb[c];
+      s += e * e;
+    }
+  }
+  double t = s;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane == 0) acc[r] += sqrt(t);
+}
+
 }  // namespace ifkv
 
 using namespace ifkv;
+
+extern "C" int ifkv_row_dist_accum(const float* a, const float* b, int rows, int d, double* acc, void* stream) {
+  IFKV_CHECK_ARG(rows >= 0 && d > 0, "row_dist_accum: bad shape");
+  if (rows == 0) return IFKV_OK;
+  IFKV_CHECK_ARG(d % 4 != 0 || ((uintptr_t)a % 16 == 0 && (uintptr_t)b % 16 == 0), "row_dist_accum: misaligned rows");
+  row_dist_accum_kernel<<<(rows + 7) / 8, 256, 0, as_stream(stream)>>>(a, b, rows, d, acc);
+  IFKV_LAUNCH_CHECK("row_dist_accum");
+  return IFKV_OK;
+}
 
 extern "C" int ifkv_add_rmsnorm(float* h, const void* delta, int delta_dtype, int n_parts, const float* gain,
                                 int rows, int d, int out_mode, void* out, void* stream) {

@@ -182,6 +182,12 @@ def embed_rows(table, ids):
     return h
 
 
+def row_dist_accum(a, b, acc):
+    """acc[r] += || a[r] - b[r] ||_2 over fp32 [rows, d] (fp64 accumulator)."""
+    rows, d = a.shape
+    N.call("ifkv_row_dist_accum", N.ptr(a), N.ptr(b), rows, d, N.ptr(acc), _s())
+
+
 def split3(x):
     torch = _torch()
     out = torch.empty((3,) + tuple(x.shape), dtype=torch.bfloat16, device=x.device)
@@ -477,13 +483,16 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
 
 
 def layer_stack(weights, token_ids, positions, k_slab, v_slab, dst_rows, horizon, want_hidden: bool = False,
-                attn_fn=None):
-    """Advance S tokens (device int64 ids/positions) through every layer.
+                attn_fn=None, n_layers: Optional[int] = None, on_hidden=None):
+    """Advance S tokens (device int64 ids/positions) through every layer
+    (or the first ``n_layers``).
 
     Layer l: x = rms_norm(h); q,k,v = x W; rope at ``positions``; k,v written
     to slab rows ``dst_rows`` (so later tokens see them); attention of q over
     slab keys 0..horizon[i]; residual O-proj and MLP.  The last layer stops
-    after its K/V (nothing else can change a K/V row).
+    after its K/V (nothing else can change a K/V row) unless the hidden state
+    is wanted; ``on_hidden(l, h)`` sees each layer's block output (fp32 [S, d],
+    model.py:450-452).
     """
     torch = _torch()
     cfg = weights.config
@@ -494,13 +503,18 @@ def layer_stack(weights, token_ids, positions, k_slab, v_slab, dst_rows, horizon
         return None  # (sharded ranks keep looping: every layer has collectives)
     bf16 = weights.precision == "bf16"
     act_mode = N.OUT_BF16 if bf16 else N.OUT_F32
+    run = cfg.n_layers if n_layers is None else int(n_layers)
+    if not 1 <= run <= cfg.n_layers:
+        raise ConfigurationError(f"n_layers {run} outside [1, {cfg.n_layers}]")
+    fused = FUSED_RESIDUAL or on_hidden is not None  # h complete after every layer
     cs = rope_table(positions, Dh, cfg.rope_base, dev)
     h = embed_rows(weights.embedding, token_ids)
     qbuf = torch.empty((S, H, Dh), dtype=weights.torch_dtype, device=dev)
     attn_out = torch.empty_like(qbuf)
     pending = None
-    for li, lw in enumerate(weights.layers):
-        final = li == cfg.n_layers - 1 and not want_hidden
+    for li in range(run):
+        lw = weights.layers[li]
+        final = li == cfg.n_layers - 1 and not want_hidden and on_hidden is None
         x = add_rmsnorm(h, pending, 1, lw.attn_norm, act_mode)
         qkv = torch.mm(x, lw.wqkv)
         esz = qkv.element_size()
@@ -514,15 +528,17 @@ def layer_stack(weights, token_ids, positions, k_slab, v_slab, dst_rows, horizon
         else:
             with _Bracket("recompute_attn", li):
                 recompute_attn(qbuf, k_slab[li], v_slab[li], horizon, H, Hkv, Dh, out=attn_out)
-        if FUSED_RESIDUAL:  # h += attn Wo inside the GEMM (fp32 C operand, beta = 1)
+        if fused:  # h += attn Wo inside the GEMM (fp32 C operand, beta = 1)
             residual_mm(h, attn_out.view(S, d), lw.wo)
             x2 = add_rmsnorm(h, None, 0, lw.mlp_norm, act_mode)
         else:
             x2 = add_rmsnorm(h, mm_f32(attn_out.view(S, d), lw.wo), 1, lw.mlp_norm, act_mode)
         gu = torch.mm(x2, lw.wgu)
         a = silu_mul(gu, 1, cfg.d_ff, act_mode)
-        if FUSED_RESIDUAL:
+        if fused:
             residual_mm(h, a, lw.wdown)
+            if on_hidden is not None:
+                on_hidden(li, h)
         else:
             pending = mm_f32(a, lw.wdown)
     if pending is not None:

@@ -164,6 +164,51 @@ def select_topk(scores, k: int):
     return idx
 
 
+def score_cacheblend(weights, chunks: Sequence[ChunkSpec], early_layers: int):
+    """CacheBlend baseline (selection.py:190-223): per context token, the L2
+    distance between its block outputs in the chunk-local runs (positions
+    0..len-1, causal inside the chunk) and in one full-context causal run,
+    summed over the first ``early_layers`` layers.  Both runs go through the
+    layer stack (chunk-local runs one chunk at a time into a scratch slab);
+    the distances accumulate on the device in fp64 (``ifkv_row_dist_accum``).
+    Returns fp64 [N] on the device."""
+    torch = _torch()
+    cfg = weights.config
+    if early_layers < 1:
+        raise ConfigurationError("early_layers must be >= 1")
+    if early_layers > cfg.n_layers:
+        raise ConfigurationError(f"early_layers {early_layers} exceeds n_layers {cfg.n_layers}")
+    if not chunks:
+        raise ConfigurationError("no chunks to score")
+    dev = weights.device
+    lens = [int(np.asarray(c.token_ids).size) for c in chunks]
+    n = sum(lens)
+    if n > cfg.max_position:
+        raise ConfigurationError(f"context length {n} exceeds max_position {cfg.max_position}")
+    toks = np.concatenate([np.asarray(c.token_ids, np.int64) for c in chunks])
+    if toks.min() < 0 or toks.max() >= cfg.vocab_size:
+        raise ConfigurationError("token id outside vocabulary")
+    local = torch.empty((early_layers, n, cfg.d_model), dtype=torch.float32, device=dev)
+    kv_shape = (early_layers, max(lens), cfg.kv_heads, cfg.d_head)
+    ks = torch.empty(kv_shape, dtype=weights.torch_dtype, device=dev)
+    vs = torch.empty_like(ks)
+    r0 = 0
+    for c, ln in zip(chunks, lens):
+        ar = torch.arange(ln, dtype=torch.int64, device=dev)
+        ids = E.h2d(np.asarray(c.token_ids, np.int64), dev)
+        E.layer_stack(weights, ids, ar, ks, vs, ar, ar, n_layers=early_layers,
+                      on_hidden=lambda li, h, r0=r0, ln=ln: local[li, r0:r0 + ln].copy_(h))
+        r0 += ln
+    del ks, vs
+    kf = torch.empty((early_layers, n, cfg.kv_heads, cfg.d_head), dtype=weights.torch_dtype, device=dev)
+    vf = torch.empty_like(kf)
+    ar = torch.arange(n, dtype=torch.int64, device=dev)
+    scores = torch.zeros(n, dtype=torch.float64, device=dev)
+    E.layer_stack(weights, E.h2d(toks, dev), ar, kf, vf, ar, ar, n_layers=early_layers,
+                  on_hidden=lambda li, h: E.row_dist_accum(local[li], h, scores))
+    return scores
+
+
 def select_epic(chunk_lengths: Sequence[int], ratio: float) -> np.ndarray:
     """First ceil(ratio * len) tokens of every chunk (selection.py:226-239)."""
     if not 0.0 <= ratio <= 1.0:
@@ -211,8 +256,12 @@ def run_selection(weights, chunks: Sequence[ChunkSpec], cache: AssembledCache, p
         sel = select_epic(cache.chunk_lengths, ratio)
     elif config.strategy is Strategy.RANDOM:
         sel = select_random(n, config.resolve_budget(n), config.seed)
-    else:
-        raise ConfigurationError("the cacheblend baseline is not on the accelerated path (SURVEY §8f row 4)")
+    else:  # CacheBlend
+        if not chunks:
+            raise ConfigurationError("no chunks to score")
+        scores = score_cacheblend(weights, chunks, config.cacheblend_layers)
+        return SelectionResult(scores=scores, selected=select_topk(scores, config.resolve_budget(n)),
+                               strategy=config.strategy.value)
     scores = np.zeros(n, np.float32)
     scores[sel] = 1.0
     return SelectionResult(scores=torch.as_tensor(scores, device=dev), selected=torch.as_tensor(sel, device=dev),

@@ -96,6 +96,12 @@ def tiny_case(out):
     for mode in ("mean", "max"):
         imps, _ = ck.score_chunks(w, chunks, prompt, budget=6, chunk_score=mode, prefilled=kvs)
         out[f"tiny_imp_{mode}"] = imps
+    # baseline selector: CacheBlend early-layer deviation (selection.py:190-223)
+    for el in (1, 2):
+        out[f"tiny_cacheblend{el}_scores"] = ck.selection.score_cacheblend(w, chunks, el)
+    cb = ck.run_selection(w, chunks, cache, prompt, ck.SelectionConfig(strategy="cacheblend", topk=6,
+                                                                        cacheblend_layers=2))
+    out["tiny_cacheblend_sel6"] = cb.selected
     # IFKC files written by the reference (f64 and f32 precision codes)
     import tempfile
 
@@ -140,6 +146,11 @@ def c1_case(out, seed):
     out[p + "reorder_perm"] = plan_r.permutation
     out[p + "reorder_imp"] = plan_r.chunk_importance
     out[p + "reorder_sel"] = second.selected
+    if seed == 0:
+        cb = ck.run_selection(w, g.chunks, cache, g.prompt_token_ids,
+                              ck.SelectionConfig(strategy="cacheblend", ratio=0.15, cacheblend_layers=2))
+        out[p + "cacheblend_scores"] = cb.scores
+        out[p + "cacheblend_selected"] = cb.selected
 
 
 def gqa_case(out):

@@ -260,3 +260,55 @@ def test_first_token_over_recomputed_cache(cuda, precision):
                              prefix=[(oc2.keys[l, :n], oc2.values[l, :n]) for l in range(oc2.n_layers)]).logits
     assert rel_err(logits.double().cpu().numpy(), want) <= 1e-4
     assert P.greedy_token(logits) == int(np.argmax(want))
+
+
+# ---------------------------------------------------------------------------
+# CacheBlend baseline selector on the GPU (selection.py:190-223)
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("early", [1, 2])
+def test_fp32_cacheblend_vs_golden(tiny, golden_small, early):
+    """fp32 mode against the reference's own scores (tiny config)."""
+    P, _, dw, _ = tiny
+    toks = golden_small["tiny_tokens"]
+    chunks = [P.ChunkSpec(f"c{i}", toks[8 * i:8 * i + 8], i) for i in range(3)]
+    s = P.score_cacheblend(dw, chunks, early).cpu().numpy()
+    assert rel_err(s, golden_small[f"tiny_cacheblend{early}_scores"]) <= 1e-4
+    if early == 2:
+        cache = P.assemble([P.prefill_chunk(dw, c) for c in chunks])
+        res = P.run_selection(dw, chunks, cache, golden_small["tiny_prompt"],
+                              P.SelectionConfig(strategy="cacheblend", topk=6, cacheblend_layers=2))
+        np.testing.assert_array_equal(res.selected_numpy(), golden_small["tiny_cacheblend_sel6"])
+
+
+def test_c1_cacheblend_vs_oracle(c1):
+    """BASELINE config 1, bf16 path, against the oracle on identical weights:
+    scores within the bf16 bar; the selected sets overlap almost entirely
+    (the bf16 hidden states move near-tied scores)."""
+    P = _pkg()
+    dw, ow, g, kvs = c1
+    s = P.score_cacheblend(dw, g.chunks, 2).cpu().numpy()
+    want = O.score_cacheblend(ow, [c.token_ids for c in g.chunks], 2)
+    assert rel_err(s, want) <= 1e-2
+    cache = P.assemble(kvs)
+    res = P.run_selection(dw, g.chunks, cache, g.prompt_token_ids,
+                          P.SelectionConfig(strategy="cacheblend", ratio=0.15, cacheblend_layers=2))
+    got = res.selected_numpy()
+    ref = O.select_topk(want, 308)
+    assert got.size == 308 and np.intersect1d(got, ref).size >= 0.95 * 308
+    # the first chunk sits at its local positions in both runs: zero deviation
+    np.testing.assert_array_equal(s[:256], np.zeros(256))
+
+
+def test_cacheblend_validation(tiny):
+    P, _, dw, _ = tiny
+    chunks = [P.ChunkSpec("a", np.arange(5), 0)]
+    with pytest.raises(P.ConfigurationError):
+        P.score_cacheblend(dw, chunks, 0)
+    with pytest.raises(P.ConfigurationError):
+        P.score_cacheblend(dw, chunks, dw.config.n_layers + 1)
+    with pytest.raises(P.ConfigurationError):
+        P.score_cacheblend(dw, [], 1)
+    s = P.score_cacheblend(dw, chunks, 2).cpu().numpy()
+    np.testing.assert_array_equal(s, np.zeros(5))

@@ -183,3 +183,26 @@ def test_oracle_c1_bf16_weights(golden_c1, seed):
     np.testing.assert_array_equal(perm, golden_c1[p + "reorder_perm"])
     np.testing.assert_allclose(imps, golden_c1[p + "reorder_imp"], rtol=1e-9)
     np.testing.assert_array_equal(sel2, golden_c1[p + "reorder_sel"])
+
+
+class TestOracleCacheBlend:
+    """Baseline selector (selection.py:190-223) pinned to the reference's scores."""
+
+    @pytest.mark.parametrize("early", [1, 2])
+    def test_tiny_scores(self, golden_small, tiny_w, early):
+        toks = golden_small["tiny_tokens"]
+        s = O.score_cacheblend(tiny_w, [toks[8 * i:8 * i + 8] for i in range(3)], early)
+        np.testing.assert_allclose(s, golden_small[f"tiny_cacheblend{early}_scores"], rtol=1e-9, atol=1e-12)
+        if early == 2:
+            np.testing.assert_array_equal(O.select_topk(s, 6), golden_small["tiny_cacheblend_sel6"])
+
+    def test_c1_scores_and_selection(self, golden_c1):
+        w = init_weights(C1, seed=7).bf16_rounded()
+        toks = golden_c1["c1s0_tokens"]
+        s = O.score_cacheblend(w, [toks[256 * i:256 * i + 256] for i in range(8)], 2)
+        np.testing.assert_allclose(s, golden_c1["c1s0_cacheblend_scores"], rtol=1e-9, atol=1e-12)
+        np.testing.assert_array_equal(O.select_topk(s, 308), golden_c1["c1s0_cacheblend_selected"])
+
+    def test_single_chunk_scores_zero(self, tiny_w):
+        s = O.score_cacheblend(tiny_w, [np.arange(10) % 64], 2)
+        np.testing.assert_array_equal(s, np.zeros(10))
