@@ -11,8 +11,9 @@ scatter.  value = context tokens / step time, summed over ranks.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Under torchrun each rank runs an independent replica (chunk sharding of one
-context is a later milestone).  Rank 0 prints one JSON line.
+Under torchrun (N > 1) the ranks chunk-shard ONE context (zig-zag chunk
+ownership, NCCL softmax-state merges, top-k candidate all-gather, sparse-query
+partial attention).  Rank 0 prints one JSON line.
 """
 
 from __future__ import annotations
@@ -41,6 +42,18 @@ except Exception:
     pass
 
 METRIC = "assemble+select+recompute ms & ctx tok/s, Llama-3-8B shape, 32K ctx, 15% recompute"
+
+# DRAM bytes per launch of the roofline kernels from one `ncu --set full`
+# capture (tools/gpu_prof.sh -> tools/ncu_traffic.py), committed under profiles/.
+TRAFFIC_FILE = ROOT / "profiles" / "r1_ncu_traffic.json"
+
+
+def ncu_traffic(name):
+    try:
+        t = json.loads(TRAFFIC_FILE.read_text())[name]
+        return t["dram_read_bytes"] + t["dram_write_bytes"]
+    except Exception:
+        return None
 
 
 def parse():
@@ -280,7 +293,8 @@ def run_ours(args, world, rank, local):
     achieved = flops_per_launch / (attn_avg_ms / 1e3) / 1e12 if attn_avg_ms else None
     peak = PEAKS["bf16_tflops_sustained"]
     roof = {"kernel": "ifkv recompute_attn (tcgen05)", "bound": "tensor", "achieved": achieved, "peak": peak,
-            "unit": "TFLOP/s", "frac": achieved / peak if achieved else None, "traffic": None,
+            "unit": "TFLOP/s", "frac": achieved / peak if achieved else None,
+            "traffic": ncu_traffic("recompute_attn_tc"), "traffic_source": f"ncu --set full, {TRAFFIC_FILE.name}",
             "peak_source": PEAKS["source"] + " sustained bf16",
             "algorithmic_flops_per_launch": flops_per_launch, "avg_launch_ms": attn_avg_ms,
             "launches_per_step": len(attn_ms), "share_of_step": float(np.sum(attn_ms)) / ms if attn_ms else None}
@@ -291,7 +305,7 @@ def run_ours(args, world, rank, local):
         ach = rot_bytes / (float(np.mean(rot_ms)) / 1e3) / 1e9
         rot_roof = {"kernel": "ifkv rotate_rows (Kernel 1)", "bound": "hbm", "achieved": ach, "peak": PEAKS["hbm_gbs"],
                     "unit": "GB/s", "frac": ach / PEAKS["hbm_gbs"], "avg_launch_ms": float(np.mean(rot_ms)),
-                    "algorithmic_bytes_per_launch": rot_bytes}
+                    "algorithmic_bytes_per_launch": rot_bytes, "traffic": ncu_traffic("rotate_rows")}
 
     sct_roof = None
     if sct:  # fused rope + K/V scatter epilogue of the QKV GEMM (bytes per launch: qkv read, q/K/V written)
@@ -299,7 +313,8 @@ def run_ours(args, world, rank, local):
         ach = b_s / (t_s / 1e3) / 1e9
         sct_roof = {"kernel": "ifkv qkv_rope_scatter", "bound": "hbm", "achieved": ach, "peak": PEAKS["hbm_gbs"],
                     "unit": "GB/s", "frac": ach / PEAKS["hbm_gbs"], "avg_launch_ms": t_s,
-                    "algorithmic_bytes_per_launch": b_s, "launches_per_step": len(sct)}
+                    "algorithmic_bytes_per_launch": b_s, "launches_per_step": len(sct),
+                    "traffic": ncu_traffic("qkv_rope_scatter")}
 
     # comparator: full bf16 prefill of the same context through the same kernels
     torch.cuda.synchronize()

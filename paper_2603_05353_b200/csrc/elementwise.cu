@@ -27,13 +27,14 @@ __device__ __forceinline__ void store_mode(void* out, int mode, int64_t part_str
   }
 }
 
-// Block-wide deterministic sum (fixed tree) for blockDim.x == 256.
-__device__ __forceinline__ float block_sum_256(float v, float* red) {
+// Block-wide deterministic sum (fixed tree) for blockDim.x == kThreads.
+template <int kThreads>
+__device__ __forceinline__ float block_sum(float v, float* red) {
   v = warp_sum(v);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   if (l == 0) red[w] = v;
   __syncthreads();
-  float t = l < 8 ? red[l] : 0.f;
+  float t = l < kThreads / 32 ? red[l] : 0.f;
   t = warp_sum(t);
   __syncthreads();
   return t;
@@ -71,13 +72,15 @@ __device__ __forceinline__ void store4_mode(void* out, int mode, int64_t part_st
 }
 
 // One CTA per row; each thread owns 4-wide vectors (d % 4 == 0), kept in
-// registers between the residual add and the normalisation (d <= 8192).
-template <typename TD>
-__global__ void __launch_bounds__(256) add_rmsnorm_kernel(float* __restrict__ h, const TD* __restrict__ delta,
-                                                          int n_parts, const float* __restrict__ gain, int rows,
-                                                          int d, int mode, void* __restrict__ out) {
-  __shared__ float red[8];
-  constexpr int kMaxVec = 8;  // 8 x 4 x 256 = 8192 elements per row
+// registers between the residual add and the normalisation
+// (d <= 8 * 4 * kThreads).  128-thread CTAs for d <= 4096: 16 rows in flight
+// per SM instead of 8 (the kernel is load-latency bound).
+template <typename TD, int kThreads>
+__global__ void __launch_bounds__(kThreads) add_rmsnorm_kernel(float* __restrict__ h, const TD* __restrict__ delta,
+                                                               int n_parts, const float* __restrict__ gain, int rows,
+                                                               int d, int mode, void* __restrict__ out) {
+  __shared__ float red[kThreads / 32];
+  constexpr int kMaxVec = 8;
   const int r = blockIdx.x;
   float* hr = h + (int64_t)r * d;
   const int64_t pstride = (int64_t)rows * d;
@@ -85,27 +88,92 @@ __global__ void __launch_bounds__(256) add_rmsnorm_kernel(float* __restrict__ h,
   float ss = 0.f;
 #pragma unroll
   for (int u = 0; u < kMaxVec; ++u) {
-    const int i = (u * 256 + threadIdx.x) * 4;
-    if (i < d) {
-      x[u] = ld4(hr + i);
-      if (n_parts > 0) {
+    const int i = (u * kThreads + threadIdx.x) * 4;
+    if (i < d) x[u] = ld4(hr + i);
+  }
+  if (n_parts > 0) {
+#pragma unroll
+    for (int u = 0; u < kMaxVec; ++u) {
+      const int i = (u * kThreads + threadIdx.x) * 4;
+      if (i < d) {
         for (int q = 0; q < n_parts; ++q) add4(x[u], ld4(delta + q * pstride + (int64_t)r * d + i));
         *reinterpret_cast<float4*>(hr + i) = x[u];
       }
-      ss += x[u].x * x[u].x + x[u].y * x[u].y + x[u].z * x[u].z + x[u].w * x[u].w;
     }
   }
+#pragma unroll
+  for (int u = 0; u < kMaxVec; ++u) {
+    const int i = (u * kThreads + threadIdx.x) * 4;
+    if (i < d) ss += x[u].x * x[u].x + x[u].y * x[u].y + x[u].z * x[u].z + x[u].w * x[u].w;
+  }
   if (!out) return;
-  float ms = block_sum_256(ss, red) / (float)d;
+  float ms = block_sum<kThreads>(ss, red) / (float)d;
   float den = sqrtf(ms + 1e-6f);
 #pragma unroll
   for (int u = 0; u < kMaxVec; ++u) {
-    const int i = (u * 256 + threadIdx.x) * 4;
+    const int i = (u * kThreads + threadIdx.x) * 4;
     if (i < d) {
       float4 g = ld4(gain + i);
       float4 y = make_float4(x[u].x / den * g.x, x[u].y / den * g.y, x[u].z / den * g.z, x[u].w / den * g.w);
       store4_mode(out, mode, pstride, (int64_t)r * d + i, y);
     }
+  }
+}
+
+// Persistent variant for d == 4 * 4 * 256 = 4096 rows (the Llama-width
+// recompute loop): a CTA walks rows r, r + grid, ... and issues the loads of
+// its next row before reducing and storing the current one, so HBM reads stay
+// in flight across the reduction barrier.
+template <typename TD>
+__global__ void __launch_bounds__(256) add_rmsnorm_pf_kernel(float* __restrict__ h, const TD* __restrict__ delta,
+                                                             int n_parts, const float* __restrict__ gain, int rows,
+                                                             int mode, void* __restrict__ out) {
+  constexpr int d = 4096, kV = 4;
+  __shared__ float red[2][8];
+  const int64_t pstride = (int64_t)rows * d;
+  float4 g[kV];
+#pragma unroll
+  for (int u = 0; u < kV; ++u) g[u] = ld4(gain + (u * 256 + threadIdx.x) * 4);
+  auto load = [&](int r, float4* x) {
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      const int i = (u * 256 + threadIdx.x) * 4;
+      x[u] = ld4(h + (int64_t)r * d + i);
+      for (int q = 0; q < n_parts; ++q) add4(x[u], ld4(delta + q * pstride + (int64_t)r * d + i));
+    }
+  };
+  float4 cur[kV], nxt[kV];
+  int r = blockIdx.x;
+  if (r < rows) load(r, cur);
+  for (int it = 0; r < rows; r += gridDim.x, ++it) {
+    const int rn = r + gridDim.x;
+    if (rn < rows) load(rn, nxt);
+    float ss = 0.f;
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      const int i = (u * 256 + threadIdx.x) * 4;
+      if (n_parts > 0) *reinterpret_cast<float4*>(h + (int64_t)r * d + i) = cur[u];
+      ss += cur[u].x * cur[u].x + cur[u].y * cur[u].y + cur[u].z * cur[u].z + cur[u].w * cur[u].w;
+    }
+    if (out) {
+      // block sum, double-buffered scratch: one barrier per row
+      ss = warp_sum(ss);
+      if ((threadIdx.x & 31) == 0) red[it & 1][threadIdx.x >> 5] = ss;
+      __syncthreads();
+      float t = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) t += red[it & 1][w];
+      const float den = sqrtf(t / (float)d + 1e-6f);
+#pragma unroll
+      for (int u = 0; u < kV; ++u) {
+        const int i = (u * 256 + threadIdx.x) * 4;
+        float4 y = make_float4(cur[u].x / den * g[u].x, cur[u].y / den * g[u].y, cur[u].z / den * g[u].z,
+                               cur[u].w / den * g[u].w);
+        store4_mode(out, mode, pstride, (int64_t)r * d + i, y);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kV; ++u) cur[u] = nxt[u];
   }
 }
 
@@ -232,11 +300,35 @@ extern "C" int ifkv_add_rmsnorm(float* h, const void* delta, int delta_dtype, in
   IFKV_CHECK_ARG(n_parts == 0 || delta_dtype == IFKV_F32 || delta_dtype == IFKV_BF16, "add_rmsnorm: bad dtype");
   if (rows == 0) return IFKV_OK;
   cudaStream_t s = as_stream(stream);
-  if (n_parts > 0 && delta_dtype == IFKV_BF16)
-    add_rmsnorm_kernel<__nv_bfloat16><<<rows, 256, 0, s>>>(h, (const __nv_bfloat16*)delta, n_parts, gain, rows, d,
-                                                           out_mode, out);
-  else
-    add_rmsnorm_kernel<float><<<rows, 256, 0, s>>>(h, (const float*)delta, n_parts, gain, rows, d, out_mode, out);
+  const bool bf = n_parts > 0 && delta_dtype == IFKV_BF16;
+#ifndef IFKV_RMS_PERSIST
+#define IFKV_RMS_PERSIST 1
+#endif
+#ifndef IFKV_RMS_PERSIST_CTAS
+#define IFKV_RMS_PERSIST_CTAS 3
+#endif
+  if (IFKV_RMS_PERSIST && d == 4096 && rows >= 148 * 4) {
+    const unsigned grid = 148 * IFKV_RMS_PERSIST_CTAS;
+    if (bf)
+      add_rmsnorm_pf_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(h, (const __nv_bfloat16*)delta, n_parts, gain, rows,
+                                                                out_mode, out);
+    else
+      add_rmsnorm_pf_kernel<float><<<grid, 256, 0, s>>>(h, (const float*)delta, n_parts, gain, rows, out_mode, out);
+  } else if (d <= 4096) {
+    if (bf)
+      add_rmsnorm_kernel<__nv_bfloat16, 128><<<rows, 128, 0, s>>>(h, (const __nv_bfloat16*)delta, n_parts, gain, rows,
+                                                                 d, out_mode, out);
+    else
+      add_rmsnorm_kernel<float, 128><<<rows, 128, 0, s>>>(h, (const float*)delta, n_parts, gain, rows, d, out_mode,
+                                                         out);
+  } else {
+    if (bf)
+      add_rmsnorm_kernel<__nv_bfloat16, 256><<<rows, 256, 0, s>>>(h, (const __nv_bfloat16*)delta, n_parts, gain, rows,
+                                                                 d, out_mode, out);
+    else
+      add_rmsnorm_kernel<float, 256><<<rows, 256, 0, s>>>(h, (const float*)delta, n_parts, gain, rows, d, out_mode,
+                                                         out);
+  }
   IFKV_LAUNCH_CHECK("add_rmsnorm");
   return IFKV_OK;
 }

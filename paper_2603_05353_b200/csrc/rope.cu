@@ -326,6 +326,54 @@ __global__ void qkv_rope_scatter_strided_kernel(const TIn* __restrict__ qkv, int
   }
 }
 
+// bf16 -> bf16, one part, Dh = 128 (the recompute loop): one pass, two
+// 16-byte vectors per thread (both loads issued first), 32-bit indexing,
+// cos/sin as two 16-byte loads.
+__global__ void __launch_bounds__(256) qkv_rope_scatter_bf16_kernel(
+    const __nv_bfloat16* __restrict__ qkv, int total, int H, int Hkv, const float2* __restrict__ cs,
+    __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ k_dst, __nv_bfloat16* __restrict__ v_dst,
+    const int64_t* __restrict__ dst_rows) {
+  const int vpr = (H + 2 * Hkv) * 16;  // 16-byte vectors per row (Dh = 128: 16 per head)
+  const int t0 = blockIdx.x * 512 + threadIdx.x;
+  uint4 val[2];
+  int r[2], c[2];
+  bool on[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int t = t0 + u * 256;
+    r[u] = t / vpr;
+    c[u] = t - r[u] * vpr;
+    on[u] = t < total && (q_out || c[u] >= H * 16);
+    if (on[u]) val[u] = *reinterpret_cast<const uint4*>(qkv + (int64_t)t * 8);
+  }
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    if (!on[u]) continue;
+    const int head = c[u] >> 4, e0 = (c[u] & 15) * 8;
+    if (head < H + Hkv) {
+      const float4* c4 = reinterpret_cast<const float4*>(cs + (int64_t)r[u] * 64 + e0 / 2);
+      const float4 ab = __ldg(c4), cd = __ldg(c4 + 1);
+      const float2 a[4] = {make_float2(ab.x, ab.y), make_float2(ab.z, ab.w), make_float2(cd.x, cd.y),
+                           make_float2(cd.z, cd.w)};
+      __nv_bfloat162* e = reinterpret_cast<__nv_bfloat162*>(&val[u]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 x = __bfloat1622float2(e[q]);
+        e[q] = __floats2bfloat162_rn(x.x * a[q].x - x.y * a[q].y, x.x * a[q].y + x.y * a[q].x);
+      }
+    }
+    __nv_bfloat16* d;
+    if (head < H) {
+      d = q_out + ((int64_t)r[u] * H + head) * 128 + e0;
+    } else {
+      const int64_t drow = dst_rows ? dst_rows[r[u]] : r[u];
+      d = head < H + Hkv ? k_dst + (drow * Hkv + (head - H)) * 128 + e0
+                         : v_dst + (drow * Hkv + (head - H - Hkv)) * 128 + e0;
+    }
+    *reinterpret_cast<uint4*>(d) = val[u];
+  }
+}
+
 }  // namespace ifkv
 
 using namespace ifkv;
@@ -429,7 +477,7 @@ extern "C" int ifkv_qkv_rope_scatter(const void* qkv, int qkv_dtype, int n_parts
   auto c = reinterpret_cast<const float2*>(cs);
   cudaStream_t s = as_stream(stream);
 #ifndef IFKV_SCATTER_ROW
-#define IFKV_SCATTER_ROW 1
+#define IFKV_SCATTER_ROW 0
 #endif
   const bool row_kernel = IFKV_SCATTER_ROW && Dh % 8 == 0 && (H + 2 * Hkv) * Dh / 8 <= 4 * 256;
   const bool strided = !row_kernel && Dh % 8 == 0;
@@ -451,6 +499,18 @@ extern "C" int ifkv_qkv_rope_scatter(const void* qkv, int qkv_dtype, int n_parts
   else                                                                                                              \
     qkv_rope_scatter_kernel<TI, TO><<<grid, 256, 0, s>>>((const TI*)qkv, n_parts, part_stride, rows, H, Hkv, Dh, c,  \
                                                          (TO*)q_out, (TO*)k_dst, (TO*)v_dst, dst_rows)
+#ifndef IFKV_SCATTER_BF16
+#define IFKV_SCATTER_BF16 1
+#endif
+  const int64_t total16 = (int64_t)rows * (H + 2 * Hkv) * Dh / 8;
+  if (IFKV_SCATTER_BF16 && qkv_dtype == IFKV_BF16 && out_dtype == IFKV_BF16 && n_parts == 1 && Dh == 128 &&
+      total16 + 512 < (int64_t)INT32_MAX) {
+    qkv_rope_scatter_bf16_kernel<<<(unsigned)((total16 + 511) / 512), 256, 0, s>>>(
+        (const __nv_bfloat16*)qkv, (int)total16, H, Hkv, c, (__nv_bfloat16*)q_out, (__nv_bfloat16*)k_dst,
+        (__nv_bfloat16*)v_dst, dst_rows);
+    IFKV_LAUNCH_CHECK("qkv_rope_scatter");
+    return IFKV_OK;
+  }
   if (qkv_dtype == IFKV_F32 && out_dtype == IFKV_F32) IFKV_QKV_LAUNCH(float, float);
   else if (qkv_dtype == IFKV_F32) IFKV_QKV_LAUNCH(float, __nv_bfloat16);
   else if (out_dtype == IFKV_F32) IFKV_QKV_LAUNCH(__nv_bfloat16, float);

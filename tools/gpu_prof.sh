@@ -1,12 +1,16 @@
 # One GPU call: timeline of a warm step, ncu launch list, ncu --set full of the main kernels.
+# NCU_KERNELS entries are name:regex:skip (skip = matching launches to pass over first).
 set -x
 mkdir -p gpurun_out/ncu
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 timeout 600 python tools/timeline.py > gpurun_out/timeline.txt 2>&1
 timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/ncu/launches.csv python bench.py --ncu --warmup 1 > /dev/null 2>&1
-for k in ${NCU_KERNELS:-rotate_rows qkv_rope_scatter_vec silu_mul_bf16x8 add_rmsnorm_kernel recompute_attn_tc prompt_attn_tc assemble_gather}; do
-  timeout 900 ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:$k -c 1 \
-    -o gpurun_out/ncu/$k -f python bench.py --ncu --warmup 1 > gpurun_out/ncu/$k.log 2>&1
+DEFAULT="recompute_attn_tc:recompute_attn_tc:1 rotate_rows:rotate_rows:0 qkv_rope_scatter:qkv_rope_scatter_vec:21 add_rmsnorm:add_rmsnorm_kernel:41 silu_mul:silu_mul_bf16x8:1 prompt_attn_tc:prompt_attn_tc:1 assemble_gather:assemble_gather:0"
+for spec in ${NCU_KERNELS:-$DEFAULT}; do
+  IFS=: read name rx skip <<< "$spec"
+  timeout 900 ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:$rx -s $skip -c 1 \
+    -o gpurun_out/ncu/$name -f python bench.py --ncu --warmup 1 > gpurun_out/ncu/$name.log 2>&1
 done
+python tools/ncu_traffic.py gpurun_out/ncu/*.ncu-rep > gpurun_out/ncu/traffic.json
 ls -la gpurun_out/ncu
