@@ -15,6 +15,7 @@ from paper_2603_05353_b200 import _native as N  # noqa: E402
 
 
 def run(lib, iters=30):
+    torch.manual_seed(0)
     N._lib = None
     N.load(Path(lib))
     from paper_2603_05353_b200 import engine as E
@@ -38,12 +39,16 @@ def run(lib, iters=30):
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / iters
     flops = 4.0 * H * Dh * float(np.sum(sel + 1))
-    return ms, flops / ms / 1e9
+    return ms, flops / ms / 1e9, out.float()
 
 
 if __name__ == "__main__":
     libs = sys.argv[1:] or [str(ROOT / "paper_2603_05353_b200/_build/libifkv.so")]
+    ref = None
     for rep in range(4):
         for lib in libs:
-            ms, tf = run(lib)
-            print(f"{lib}: {ms:.3f} ms  {tf:.0f} TFLOP/s", flush=True)
+            ms, tf, out = run(lib)
+            if ref is None:
+                ref = out
+            err = float((out - ref).abs().max() / ref.abs().max())
+            print(f"{lib}: {ms:.3f} ms  {tf:.0f} TFLOP/s  (max rel diff vs first lib {err:.1e})", flush=True)
