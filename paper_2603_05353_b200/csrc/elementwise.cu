@@ -234,6 +234,51 @@ __global__ void silu_mul_bf16x8_kernel(const __nv_bfloat16* __restrict__ gu, int
   }
 }
 
+// silu(g) = g * sigmoid(g) = 0.5 g (1 + tanh(g / 2)): one MUFU.TANH per
+// element (tanh.approx.f32, rel. error ~2^-11, below the bf16 output rounding).
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// bf16 -> bf16, one part: one pass (no grid-stride loop), two 8-element
+// vectors per thread with all four 16-byte loads issued first, 32-bit indexing.
+__global__ void __launch_bounds__(256) silu_mul_bf16_fast_kernel(const __nv_bfloat16* __restrict__ gu, int total,
+                                                                 int vpr, __nv_bfloat16* __restrict__ out) {
+  const int t0 = blockIdx.x * 512 + threadIdx.x;
+  uint4 gv[2], uv[2];
+  int r[2], c[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int t = t0 + u * 256;
+    r[u] = t / vpr;
+    c[u] = t - r[u] * vpr;
+    if (t < total) {
+      const __nv_bfloat16* base = gu + (int64_t)r[u] * 16 * vpr + c[u] * 8;
+      gv[u] = *reinterpret_cast<const uint4*>(base);
+      uv[u] = *reinterpret_cast<const uint4*>(base + 8 * vpr);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    if (t0 + u * 256 >= total) continue;
+    const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv[u]);
+    const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&uv[u]);
+    uint4 ov;
+    uint32_t* o = reinterpret_cast<uint32_t*>(&ov);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 g = __bfloat1622float2(g2[k]), up = __bfloat1622float2(u2[k]);
+      const float s0 = 0.5f * g.x * (1.f + tanh_approx(0.5f * g.x));
+      const float s1 = 0.5f * g.y * (1.f + tanh_approx(0.5f * g.y));
+      __nv_bfloat162 y = __floats2bfloat162_rn(s0 * up.x, s1 * up.y);
+      o[k] = *reinterpret_cast<uint32_t*>(&y);
+    }
+    *reinterpret_cast<uint4*>(out + (int64_t)r[u] * 8 * vpr + c[u] * 8) = ov;
+  }
+}
+
 template <typename T>
 __global__ void embed_rows_kernel(const T* __restrict__ table, const int64_t* __restrict__ ids, int rows, int d,
                                   float* __restrict__ h) {
@@ -341,7 +386,15 @@ extern "C" int ifkv_silu_mul(const void* gu, int gu_dtype, int n_parts, int rows
   if (n == 0) return IFKV_OK;
   int64_t want = (n + 255) / 256;
   unsigned grid = (unsigned)(want < 148 * 16 ? want : 148 * 16);
-  if (gu_dtype == IFKV_BF16 && n_parts == 1 && out_mode == IFKV_OUT_BF16 && d_ff % 8 == 0) {
+#ifndef IFKV_SILU_FAST
+#define IFKV_SILU_FAST 1
+#endif
+  if (IFKV_SILU_FAST && gu_dtype == IFKV_BF16 && n_parts == 1 && out_mode == IFKV_OUT_BF16 && d_ff % 8 == 0 &&
+      (int64_t)rows * d_ff / 8 + 512 < (int64_t)INT32_MAX) {
+    const int total = (int)((int64_t)rows * d_ff / 8);
+    silu_mul_bf16_fast_kernel<<<(unsigned)((total + 511) / 512), 256, 0, as_stream(stream)>>>(
+        (const __nv_bfloat16*)gu, total, d_ff / 8, (__nv_bfloat16*)out);
+  } else if (gu_dtype == IFKV_BF16 && n_parts == 1 && out_mode == IFKV_OUT_BF16 && d_ff % 8 == 0) {
     const int64_t nv = (int64_t)rows * d_ff / 8;
     const int64_t w8 = (nv + 255) / 256;
     silu_mul_bf16x8_kernel<<<(unsigned)(w8 < 148 * 16 ? w8 : 148 * 16), 256, 0, as_stream(stream)>>>(

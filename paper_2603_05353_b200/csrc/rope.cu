@@ -467,7 +467,7 @@ extern "C" int ifkv_rotate_queries(const float* q, int G, int M, int H, int Dh, 
 extern "C" int ifkv_qkv_rope_scatter(const void* qkv, int qkv_dtype, int n_parts, int rows, int H, int Hkv, int Dh,
                                      const float* cs, int out_dtype, void* q_out, void* k_dst, void* v_dst,
                                      const int64_t* dst_rows, void* stream) {
-  IFKV_CHECK_ARG(Dh % 2 == 0 && H % Hkv == 0 && n_parts >= 1, "qkv_rope_scatter: bad shape");
+  IFKV_CHECK_ARG(Dh % 2 == 0 && Hkv > 0 && H >= 0 && H % Hkv == 0 && n_parts >= 1, "qkv_rope_scatter: bad shape");
   IFKV_CHECK_ARG(qkv_dtype == IFKV_F32 || qkv_dtype == IFKV_BF16, "qkv_rope_scatter: bad qkv dtype");
   IFKV_CHECK_ARG(out_dtype == IFKV_F32 || out_dtype == IFKV_BF16, "qkv_rope_scatter: bad out dtype");
   if (rows <= 0) return IFKV_OK;

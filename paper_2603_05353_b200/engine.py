@@ -516,13 +516,14 @@ def layer_stack(weights, token_ids, positions, k_slab, v_slab, dst_rows, horizon
         lw = weights.layers[li]
         final = li == cfg.n_layers - 1 and not want_hidden and on_hidden is None
         x = add_rmsnorm(h, pending, 1, lw.attn_norm, act_mode)
-        qkv = torch.mm(x, lw.wqkv)
-        esz = qkv.element_size()
-        moved = S * ((2 * Hkv * Dh) * 2 + (0 if final else 2 * H * Dh)) * esz  # read + write (q skipped when final)
-        with _Bracket("qkv_rope_scatter", moved):
-            qkv_rope_scatter(qkv, 1, H, Hkv, Dh, cs, None if final else qbuf, k_slab[li], v_slab[li], dst_rows)
-        if final:
+        if final:  # the last layer only contributes K/V: project k, v only
+            kv = torch.mm(x, lw.wqkv[:, H * Dh:])
+            with _Bracket("qkv_rope_scatter", S * 2 * Hkv * Dh * 2 * kv.element_size()):
+                qkv_rope_scatter(kv, 1, 0, Hkv, Dh, cs, None, k_slab[li], v_slab[li], dst_rows)
             return None
+        qkv = torch.mm(x, lw.wqkv)
+        with _Bracket("qkv_rope_scatter", S * (2 * Hkv * Dh + H * Dh) * 2 * qkv.element_size()):
+            qkv_rope_scatter(qkv, 1, H, Hkv, Dh, cs, qbuf, k_slab[li], v_slab[li], dst_rows)
         if attn_fn is not None:  # chunk-sharded: attention over every rank's keys
             attn_out = attn_fn(li, qbuf, k_slab[li], v_slab[li])
         else:

@@ -42,9 +42,33 @@ def run(lib):
     return [(t0, b0 / t0 / 1e6), (t1, b1 / t1 / 1e6)]
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--silu" not in sys.argv:
     for rep in range(2):
         for lib in sys.argv[1:]:
             r = run(lib)
             print(f"{lib}: rmsnorm {r[0][0] * 1e3:.1f} us {r[0][1]:.0f} GB/s | add+rmsnorm {r[1][0] * 1e3:.1f} us "
                   f"{r[1][1]:.0f} GB/s", flush=True)
+
+
+def silu(lib):
+    N._lib = None
+    N._fns.clear()
+    N.load(Path(lib))
+    from paper_2603_05353_b200 import engine as E
+
+    torch.manual_seed(0)
+    S, dff = 4916, 14336
+    gu = torch.randn(S, 2 * dff, device="cuda", dtype=torch.bfloat16)
+    t = timed(lambda: E.silu_mul(gu, 1, dff, N.OUT_BF16))
+    out = E.silu_mul(gu, 1, dff, N.OUT_BF16).float()
+    g, u = gu[:, :dff].float(), gu[:, dff:].float()
+    ref = torch.nn.functional.silu(g) * u
+    err = float((out - ref).abs().max() / ref.abs().max())
+    return t, S * dff * 6 / t / 1e6, err
+
+
+if __name__ == "__main__" and "--silu" in sys.argv:
+    for rep in range(2):
+        for lib in [a for a in sys.argv[1:] if a != "--silu"]:
+            t, gbs, err = silu(lib)
+            print(f"{lib}: silu_mul {t * 1e3:.1f} us {gbs:.0f} GB/s rel err {err:.1e}", flush=True)
