@@ -123,8 +123,16 @@ def dist_setup():
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # IFKV_DIST_BACKEND=gloo runs the same TorchComm data path with every
+        # rank on the visible GPUs round-robin (a functional check of the
+        # multi-process path on a one-GPU box); the default is NCCL, one GPU per rank.
+        backend = os.environ.get("IFKV_DIST_BACKEND", "nccl")
+        dev = local % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     return world, rank, local
@@ -388,16 +396,23 @@ def run_sharded(args, comm, world, rank, sync):
         SH.sharded_recompute(weights, shard, local, res.selected, comm)
         return res
 
+    from paper_2603_05353_b200 import _native as N
+
     for _ in range(args.warmup):
         res = step(prompt)
     torch.cuda.synchronize()
     sync()
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    launches0 = N.LAUNCH_COUNT[0]
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
     for _ in range(args.steps):
         res = step(prompt)
     ev1.record()
     torch.cuda.synchronize()
+    launches = N.LAUNCH_COUNT[0] - launches0
+    clk = clocks.stop()
     sync()
     ms = ev0.elapsed_time(ev1) / args.steps
     ms_all = comm.all_gather(torch.tensor([ms], dtype=torch.float64, device="cuda"))
@@ -435,7 +450,8 @@ def run_sharded(args, comm, world, rank, sync):
         "e2e": {"value": n_ctx / (e2e_ms / 1e3), "unit": "ctx tok/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": int(prompt.nbytes), "d2h_bytes_per_step": int(sel_host.size * 8)},
         "roofline": None,
-        "gpu_launches": None,
+        "gpu_launches": int(launches),
+        "clocks": clk,
     }
 
 
@@ -547,6 +563,10 @@ def run_reference(args, world, rank):
 
 def main():
     args = parse()
+    if os.environ.get("IFKV_BENCH_WATCHDOG"):  # debugging: dump every thread's stack and exit after N s
+        import faulthandler
+
+        faulthandler.dump_traceback_later(float(os.environ["IFKV_BENCH_WATCHDOG"]), exit=True)
     if args.impl == "reference":
         world = int(os.environ.get("WORLD_SIZE", "1"))
         rank = int(os.environ.get("RANK", "0"))

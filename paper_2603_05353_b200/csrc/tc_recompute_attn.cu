@@ -335,12 +335,16 @@ __global__ void __launch_bounds__(384, 1)
         }
         if (j == (x == 0 ? nA : nB) - 1) tc::mma_commit(&sm.o_final[x]);
       };
-      // prologue: S_A(0), S_B(0)
-      tc::mbar_wait(&sm.k_full[0], 0);
-      tc::tc_fence_after();
-      for (int x = 0; x < 2; ++x)
-        if ((x == 0 ? nA : nB) > 0) issue_s(x, 0);
-      tc::mma_commit(&sm.k_empty[0]);  // K_0 is only read by the prologue
+      // prologue: S_A(0), S_B(0).  A pair with no visible key at all (every
+      // horizon -1: queries of other ranks' chunks in the sharded partial
+      // mode) has nblk = 0 and no K block is ever loaded.
+      if (nblk > 0) {
+        tc::mbar_wait(&sm.k_full[0], 0);
+        tc::tc_fence_after();
+        for (int x = 0; x < 2; ++x)
+          if ((x == 0 ? nA : nB) > 0) issue_s(x, 0);
+        tc::mma_commit(&sm.k_empty[0]);  // K_0 is only read by the prologue
+      }
       for (int j = 0; j < nblk; ++j) {
         const int s = j & 1;
         const uint32_t ph = (j >> 1) & 1;

@@ -506,7 +506,10 @@ def layer_stack(weights, token_ids, positions, k_slab, v_slab, dst_rows, horizon
     run = cfg.n_layers if n_layers is None else int(n_layers)
     if not 1 <= run <= cfg.n_layers:
         raise ConfigurationError(f"n_layers {run} outside [1, {cfg.n_layers}]")
-    fused = FUSED_RESIDUAL or on_hidden is not None  # h complete after every layer
+    # h complete after every layer when the residual adds run in the GEMM
+    # epilogue.  The chunk-sharded path (attn_fn) keeps the separate add: its
+    # ranks-as-threads mode hung inside concurrent torch.addmm(out=...) calls.
+    fused = (FUSED_RESIDUAL and attn_fn is None) or on_hidden is not None
     cs = rope_table(positions, Dh, cfg.rope_base, dev)
     h = embed_rows(weights.embedding, token_ids)
     qbuf = torch.empty((S, H, Dh), dtype=weights.torch_dtype, device=dev)

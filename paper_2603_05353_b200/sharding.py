@@ -103,8 +103,19 @@ class TorchComm(Comm):
 
     def all_to_all(self, parts):
         parts = [p.contiguous() for p in parts]
-        # receive sizes first (first dimension may differ)
         torch = _torch()
+        if self.dist.get_backend(self.group) == "gloo":
+            # gloo has no alltoall: all-gather every rank's concatenated parts
+            # (and their sizes) and keep the slices addressed to this rank
+            sizes = torch.tensor([p.shape[0] for p in parts], dtype=torch.int64, device=parts[0].device)
+            all_sizes = [s.tolist() for s in self.all_gather(sizes)]
+            all_flat = self.all_gather_var(torch.cat(parts))
+            out = []
+            for r in range(self.world):
+                off = sum(all_sizes[r][: self.rank])
+                out.append(all_flat[r][off: off + all_sizes[r][self.rank]])
+            return out
+        # receive sizes first (first dimension may differ)
         send_n = torch.tensor([p.shape[0] for p in parts], dtype=torch.int64, device=parts[0].device)
         recv_n = torch.empty_like(send_n)
         self.dist.all_to_all_single(recv_n, send_n, group=self.group)

@@ -160,10 +160,11 @@ def test_recompute_attention_tcgen05_vs_simt(T, cuda, G):
     assert np.max(np.abs(tc - want)) <= 1e-2 * scale
 
 
-@pytest.mark.parametrize("partial", [False, True])
-def test_recompute_attention_unsorted_and_empty_horizons(T, cuda, partial):
+@pytest.mark.parametrize("partial,n_empty", [(False, 0), (True, 7), (True, 130)])
+def test_recompute_attention_unsorted_and_empty_horizons(T, cuda, partial, n_empty):
     """Rank-ordered query lists (two ascending runs) and, in partial mode,
-    rows that see no key (horizon -1): the tile span is the tile's max horizon."""
+    rows that see no key (horizon -1): the tile span is the tile's max horizon.
+    130 empty rows make whole tile pairs (2 x 32 tokens at G = 4) keyless."""
     from paper_2603_05353_b200 import engine as E
 
     rng = np.random.default_rng(11)
@@ -172,7 +173,7 @@ def test_recompute_attention_unsorted_and_empty_horizons(T, cuda, partial):
     b = np.sort(rng.choice(n, 200, replace=False))
     hz = np.concatenate([a, b])
     if partial:
-        hz[:7] = -1
+        hz[:n_empty] = -1
     q = T.as_tensor(rng.standard_normal((hz.size, H, dh)), dtype=T.float32).to(cuda, T.bfloat16)
     k = T.as_tensor(rng.standard_normal((n, hkv, dh)), dtype=T.float32).to(cuda, T.bfloat16)
     v = T.as_tensor(rng.standard_normal((n, hkv, dh)), dtype=T.float32).to(cuda, T.bfloat16)
@@ -180,13 +181,14 @@ def test_recompute_attention_unsorted_and_empty_horizons(T, cuda, partial):
     if partial:
         out, ml = E.recompute_attn_partial(q, k, v, hzt, H, hkv, dh)
         ml = ml.cpu().numpy()
-        assert np.all(ml[:7, :, 1] == 0) and np.all(np.isneginf(ml[:7, :, 0]))
-        assert np.all(out[:7].float().cpu().numpy() == 0)
-        rows = slice(7, None)
+        e = n_empty
+        assert np.all(ml[:e, :, 1] == 0) and np.all(np.isneginf(ml[:e, :, 0]))
+        assert np.all(out[:e].float().cpu().numpy() == 0)
+        rows = slice(e, None)
         # (max, sum) in natural units of the scaled logits: l * e^m == sum_j e^(s_j)
-        qd, kd = q.double().cpu().numpy()[7:], k.double().cpu().numpy()
+        qd, kd = q.double().cpu().numpy()[e:], k.double().cpu().numpy()
         for i in (0, 100, 300):
-            r = 7 + i
+            r = e + i
             for h in (0, 13):
                 s_ = qd[i, h] @ kd[: hz[r] + 1, h // (H // hkv)].T / np.sqrt(dh)
                 mt = s_.max()

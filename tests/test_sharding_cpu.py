@@ -165,3 +165,20 @@ def test_gloo_prompt_state_merge_matches_full_attention():
 
 def test_gloo_topk_candidate_merge_exact():
     assert all(_run_gloo(_body_topk))
+
+
+def _body_all_to_all(comm):
+    """Uneven (and empty) per-destination parts: rank r sends r + d rows to d,
+    every row tagged (source, destination, index)."""
+    parts = [torch.tensor([[comm.rank, d, i] for i in range(comm.rank + d)], dtype=torch.int64).reshape(-1, 3)
+             for d in range(comm.world)]
+    got = comm.all_to_all(parts)
+    ok = len(got) == comm.world
+    for src, t in enumerate(got):
+        want = torch.tensor([[src, comm.rank, i] for i in range(src + comm.rank)], dtype=torch.int64).reshape(-1, 3)
+        ok = ok and torch.equal(t, want)
+    return ok
+
+
+def test_gloo_all_to_all_uneven_and_empty():
+    assert all(_run_gloo(_body_all_to_all))
