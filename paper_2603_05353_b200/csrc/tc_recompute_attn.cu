@@ -91,7 +91,8 @@ __device__ __forceinline__ int tile_blocks_warp(const int64_t* horizon, int t0, 
 }
 
 // Softmax + epilogue of one tile; `x` = 0 (A) or 1 (B).
-__device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int nblk, int t0, int S, int H, int G,
+__device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int nblk, int b0, int t0, int S, int H,
+                                             int G,
                                              int g, const int64_t* __restrict__ horizon, float scale_log2,
                                              __nv_bfloat16* __restrict__ out, float* __restrict__ ml_out) {
   const int w = (threadIdx.x >> 5) & 3;  // lane quarter of TMEM this warp may access
@@ -116,7 +117,7 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
     if (lane == 0 && w == 0) TRACE(x * 3 + 2, clock64());
     continue;
 #endif
-    const int j0 = j * kKeys;
+    const int j0 = (b0 + j) * kKeys;  // absolute first key of the block
     const bool masked = __any_sync(0xffffffffu, j0 + kKeys - 1 > hz);
     float v[64];
     // pass 1: row max over the block (two 64-column halves)
@@ -274,8 +275,15 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
-  const int nA = sm.n_blocks[0], nB = sm.n_blocks[1];
+  // key split (gridDim.z > 1 when the grid alone would not fill the GPU):
+  // split s takes blocks [b0, b1) of the pair's span; partial outputs
+  const int n_full = max(sm.n_blocks[0], sm.n_blocks[1]);
+  const int b0 = (int)((int64_t)blockIdx.z * n_full / gridDim.z);
+  const int b1 = (int)((int64_t)(blockIdx.z + 1) * n_full / gridDim.z);
+  const int nA = max(0, min(sm.n_blocks[0], b1) - b0), nB = max(0, min(sm.n_blocks[1], b1) - b0);
   const int nblk = max(nA, nB);
+  out += (int64_t)blockIdx.z * S * H * kDh;
+  if (ml_out) ml_out += (int64_t)blockIdx.z * S * H * 2;
 
   if (warp < 4) {
 #if IFKV_ATTN_SETMAXNREG
@@ -297,12 +305,12 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t ph = (j >> 1) & 1;
         tc::mbar_wait(&sm.k_empty[s], ph ^ 1);
         tc::mbar_arrive_expect_tx(&sm.k_full[s], kTile);
-        tc::tma_load_2d(sm.k[s], &tm_k, &sm.k_full[s], g * kDh, j * kKeys);
-        tc::tma_load_2d(sm.k[s] + kPanel, &tm_k, &sm.k_full[s], g * kDh + 64, j * kKeys);
+        tc::tma_load_2d(sm.k[s], &tm_k, &sm.k_full[s], g * kDh, (b0 + j) * kKeys);
+        tc::tma_load_2d(sm.k[s] + kPanel, &tm_k, &sm.k_full[s], g * kDh + 64, (b0 + j) * kKeys);
         tc::mbar_wait(&sm.v_empty[s], ph ^ 1);
         tc::mbar_arrive_expect_tx(&sm.v_full[s], kTile);
-        tc::tma_load_2d(sm.v[s], &tm_v, &sm.v_full[s], g * kDh, j * kKeys);
-        tc::tma_load_2d(sm.v[s] + kPanel, &tm_v, &sm.v_full[s], g * kDh + 64, j * kKeys);
+        tc::tma_load_2d(sm.v[s], &tm_v, &sm.v_full[s], g * kDh, (b0 + j) * kKeys);
+        tc::tma_load_2d(sm.v[s] + kPanel, &tm_v, &sm.v_full[s], g * kDh + 64, (b0 + j) * kKeys);
       }
     } else if (warp == 1 && lane == 0) {
       constexpr uint32_t idesc_qk = tc::idesc_bf16(128, 128, 0, 0);
@@ -386,11 +394,45 @@ __global__ void __launch_bounds__(384, 1)
     const int x = (warp - 4) >> 2;  // 0: tile A (warps 4-7), 1: tile B (warps 8-11)
     const int nx = x == 0 ? nA : nB;
     const int tx = x == 0 ? tA : tB;
-    if (tx < S) softmax_tile(sm, tmem, x, nx, tx, S, H, G, g, horizon, scale_log2, out, ml_out);
+    if (tx < S) softmax_tile(sm, tmem, x, nx, b0, tx, S, H, G, g, horizon, scale_log2, out, ml_out);
   }
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 2) tc::tmem_dealloc<kTmemCols>(tmem);
+}
+
+// Combine P key-split partials (bf16 O/l normalised per split, (m, l) in
+// natural units): one warp per (token, head) row, 4 dims per lane.
+__global__ void attn_split_merge_kernel(const __nv_bfloat16* __restrict__ part_o, const float* __restrict__ part_ml,
+                                        int P, int64_t rows, __nv_bfloat16* __restrict__ out,
+                                        float* __restrict__ ml_out) {
+  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  float M = -INFINITY;
+  for (int p = 0; p < P; ++p) M = fmaxf(M, part_ml[2 * (p * rows + r)]);
+  float L = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int p = 0; p < P; ++p) {
+    const float m = part_ml[2 * (p * rows + r)];
+    const float w = m == -INFINITY ? 0.f : part_ml[2 * (p * rows + r) + 1] * __expf(m - M);
+    L += w;
+    const uint2 u = *reinterpret_cast<const uint2*>(part_o + (p * rows + r) * kDh + lane * 4);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+    acc[0] += w * a.x;
+    acc[1] += w * a.y;
+    acc[2] += w * b.x;
+    acc[3] += w * b.y;
+  }
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  uint2 o;
+  o.x = tc::pack_bf16(acc[0] * inv, acc[1] * inv);
+  o.y = tc::pack_bf16(acc[2] * inv, acc[3] * inv);
+  *reinterpret_cast<uint2*>(out + r * kDh + lane * 4) = o;
+  if (ml_out && lane == 0) {
+    ml_out[2 * r] = M;
+    ml_out[2 * r + 1] = L;
+  }
 }
 
 }  // namespace
@@ -401,6 +443,18 @@ using namespace ifkv;
 extern "C" int ifkv_recompute_attn_tc_supported(int dtype, int H, int Hkv, int Dh) {
   if (dtype != IFKV_BF16 || Dh != kDh || Hkv <= 0 || H % Hkv) return 0;
   return H / Hkv <= 16 ? 1 : 0;  // a tile holds floor(128 / G) tokens x G heads
+}
+
+// Key splits for a grid of `ctas` CTAs on `sms` SMs: none while the grid
+// fills two waves, else enough (<= 4) to reach two waves.
+static int attn_key_splits(int ctas, int sms) {
+#ifdef IFKV_ATTN_SPLITS
+  return IFKV_ATTN_SPLITS;
+#else
+  if (ctas >= 2 * sms) return 1;
+  const int p = (2 * sms + ctas - 1) / ctas;
+  return p < 4 ? p : 4;
+#endif
 }
 
 extern "C" int ifkv_recompute_attn_tc(const void* q, const void* k_layer, const void* v_layer, const int64_t* horizon,
@@ -431,11 +485,33 @@ extern "C" int ifkv_recompute_attn_tc(const void* q, const void* k_layer, const 
                                       (int)smem),
                  "recompute_attn_tc: smem attribute");
   const int tok_per_pair = 2 * (kRows / G);
-  dim3 grid(Hkv, (S + tok_per_pair - 1) / tok_per_pair);
+  const int pairs = (S + tok_per_pair - 1) / tok_per_pair;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int P = attn_key_splits(Hkv * pairs, sms);
   const float scale_log2 = scale * 1.4426950408889634f;
-  recompute_attn_tc_kernel<<<grid, 384, smem, as_stream(stream)>>>(tq, tk, tv, horizon, S, H, Hkv, scale_log2,
-                                                                    (__nv_bfloat16*)out, ml_out);
-  IFKV_LAUNCH_CHECK("recompute_attn_tc");
+  cudaStream_t st = as_stream(stream);
+  if (P == 1) {
+    recompute_attn_tc_kernel<<<dim3(Hkv, pairs, 1), 384, smem, st>>>(tq, tk, tv, horizon, S, H, Hkv, scale_log2,
+                                                                     (__nv_bfloat16*)out, ml_out);
+    IFKV_LAUNCH_CHECK("recompute_attn_tc");
+    return IFKV_OK;
+  }
+  // key-split partials in a stream-ordered scratch allocation, then one merge
+  const int64_t rows = (int64_t)S * H;
+  void* ws = nullptr;
+  const size_t o_bytes = (size_t)P * rows * kDh * 2, ml_bytes = (size_t)P * rows * 2 * 4;
+  IFKV_CUDA_CALL(cudaMallocAsync(&ws, o_bytes + ml_bytes, st), "recompute_attn_tc: split workspace");
+  auto* part_o = reinterpret_cast<__nv_bfloat16*>(ws);
+  auto* part_ml = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + o_bytes);
+  recompute_attn_tc_kernel<<<dim3(Hkv, pairs, P), 384, smem, st>>>(tq, tk, tv, horizon, S, H, Hkv, scale_log2,
+                                                                   part_o, part_ml);
+  IFKV_LAUNCH_CHECK("recompute_attn_tc (split)");
+  attn_split_merge_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(part_o, part_ml, P, rows,
+                                                                        (__nv_bfloat16*)out, ml_out);
+  IFKV_LAUNCH_CHECK("recompute_attn_tc (merge)");
+  IFKV_CUDA_CALL(cudaFreeAsync(ws, st), "recompute_attn_tc: free split workspace");
   return IFKV_OK;
 }
 

@@ -1,6 +1,7 @@
 """A/B microbenchmark of the recompute-attention kernel at the C2 shape:
 4916 selected queries (uniform over 32768 positions) x 32 heads, 8 kv heads,
 Dh 128, one layer.  Usage: python tools/attn_bench.py [lib.so ...]"""
+import os
 import sys
 import time
 from pathlib import Path
@@ -21,7 +22,7 @@ def run(lib, iters=30):
     from paper_2603_05353_b200 import engine as E
 
     rng = np.random.default_rng(0)
-    n, k, H, Hkv, Dh = 32768, 4916, 32, 8, 128
+    n, k, H, Hkv, Dh = 32768, int(os.environ.get("ATTN_K", "4916")), 32, 8, 128
     sel = np.sort(rng.choice(n, k, replace=False))
     q = torch.randn(k, H, Dh, device="cuda", dtype=torch.bfloat16)
     kk = torch.randn(n, Hkv, Dh, device="cuda", dtype=torch.bfloat16)
