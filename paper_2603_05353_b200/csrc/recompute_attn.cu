@@ -108,6 +108,34 @@ extern "C" int ifkv_recompute_attn_tc(const void* q, const void* k_layer, const 
                                       int S, int H, int Hkv, int Dh, int n_rows, float scale, void* out, float* ml_out,
                                       void* stream);
 
+extern "C" int ifkv_recompute_attn_tc_v4(const void* q, const void* k_layer, const void* v_layer,
+                                         const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows,
+                                         float scale, void* out, float* ml_out, void* stream);
+// tcgen05 kernel generation: v2 (two ping-ponging tiles per CTA) while its
+// grid fills two waves of the GPU, else v4 (one tile per CTA, double-buffered
+// S, column-split softmax: twice the CTAs; measured 0.474 vs 0.574 ms at
+// k = 1639, 0.650 vs 0.624 ms at k = 2458).  IFKV_ATTN_GEN=2/4 pins one (A/B).
+#ifndef IFKV_ATTN_GEN
+#define IFKV_ATTN_GEN 0
+#endif
+static int recompute_attn_tc_any(const void* q, const void* k_layer, const void* v_layer, const int64_t* horizon,
+                                 int S, int H, int Hkv, int Dh, int n_rows, float scale, void* out, float* ml_out,
+                                 void* stream) {
+  int gen = IFKV_ATTN_GEN;
+  if (gen == 0) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int per_pair = Hkv > 0 && H % Hkv == 0 ? 2 * (128 / (H / Hkv)) : 1;
+    const int64_t pairs = ((int64_t)S + per_pair - 1) / per_pair;
+    gen = (int64_t)Hkv * pairs >= 2 * sms ? 2 : 4;
+  }
+  if (gen == 4)
+    return ifkv_recompute_attn_tc_v4(q, k_layer, v_layer, horizon, S, H, Hkv, Dh, n_rows, scale, out, ml_out,
+                                     stream);
+  return ifkv_recompute_attn_tc(q, k_layer, v_layer, horizon, S, H, Hkv, Dh, n_rows, scale, out, ml_out, stream);
+}
+
 static int recompute_attn_simt_impl(int dtype, const void* q, const void* k_layer, const void* v_layer,
                                     const int64_t* horizon, int S, int H, int Hkv, int Dh, float scale, void* out,
                                     float* ml_out, void* stream) {
@@ -142,7 +170,7 @@ extern "C" int ifkv_recompute_attn(int dtype, const void* q, const void* k_layer
                                    const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows, float scale,
                                    void* out, void* stream) {
   if (ifkv_recompute_attn_tc_supported(dtype, H, Hkv, Dh))
-    return ifkv_recompute_attn_tc(q, k_layer, v_layer, horizon, S, H, Hkv, Dh, n_rows, scale, out, nullptr, stream);
+    return recompute_attn_tc_any(q, k_layer, v_layer, horizon, S, H, Hkv, Dh, n_rows, scale, out, nullptr, stream);
   return recompute_attn_simt_impl(dtype, q, k_layer, v_layer, horizon, S, H, Hkv, Dh, scale, out, nullptr, stream);
 }
 
@@ -152,6 +180,6 @@ extern "C" int ifkv_recompute_attn_partial(int dtype, const void* q, const void*
   IFKV_CHECK_ARG(ml_out != nullptr, "recompute_attn_partial: ml_out required");
   if (n_rows <= 0) return IFKV_ERR_ARG;
   if (ifkv_recompute_attn_tc_supported(dtype, H, Hkv, Dh))
-    return ifkv_recompute_attn_tc(q, k_layer, v_layer, horizon, S, H, Hkv, Dh, n_rows, scale, out, ml_out, stream);
+    return recompute_attn_tc_any(q, k_layer, v_layer, horizon, S, H, Hkv, Dh, n_rows, scale, out, ml_out, stream);
   return recompute_attn_simt_impl(dtype, q, k_layer, v_layer, horizon, S, H, Hkv, Dh, scale, out, ml_out, stream);
 }
