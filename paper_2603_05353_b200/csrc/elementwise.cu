@@ -75,12 +75,11 @@ __device__ __forceinline__ void store4_mode(void* out, int mode, int64_t part_st
 // registers between the residual add and the normalisation
 // (d <= 8 * 4 * kThreads).  128-thread CTAs for d <= 4096: 16 rows in flight
 // per SM instead of 8 (the kernel is load-latency bound).
-template <typename TD, int kThreads>
+template <typename TD, int kThreads, int kMaxVec = 8>
 __global__ void __launch_bounds__(kThreads) add_rmsnorm_kernel(float* __restrict__ h, const TD* __restrict__ delta,
                                                                int n_parts, const float* __restrict__ gain, int rows,
                                                                int d, int mode, void* __restrict__ out) {
   __shared__ float red[kThreads / 32];
-  constexpr int kMaxVec = 8;
   const int r = blockIdx.x;
   float* hr = h + (int64_t)r * d;
   const int64_t pstride = (int64_t)rows * d;
@@ -359,6 +358,13 @@ extern "C" int ifkv_add_rmsnorm(float* h, const void* delta, int delta_dtype, in
                                                                 out_mode, out);
     else
       add_rmsnorm_pf_kernel<float><<<grid, 256, 0, s>>>(h, (const float*)delta, n_parts, gain, rows, out_mode, out);
+  } else if (rows < 2 * 148 && d <= 4 * 2 * 1024) {  // few rows (prompt forward): spread each row over 1024 threads
+    if (bf)
+      add_rmsnorm_kernel<__nv_bfloat16, 1024, 2><<<rows, 1024, 0, s>>>(h, (const __nv_bfloat16*)delta, n_parts, gain,
+                                                                      rows, d, out_mode, out);
+    else
+      add_rmsnorm_kernel<float, 1024, 2><<<rows, 1024, 0, s>>>(h, (const float*)delta, n_parts, gain, rows, d,
+                                                              out_mode, out);
   } else if (d <= 4096) {
     if (bf)
       add_rmsnorm_kernel<__nv_bfloat16, 128><<<rows, 128, 0, s>>>(h, (const __nv_bfloat16*)delta, n_parts, gain, rows,
