@@ -105,6 +105,9 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
   const uint32_t t_s = tmem + 256 * x + lane_off;
   const uint32_t t_o = t_s + 128;
   float m_used = -INFINITY, l = 0.f;
+#ifdef IFKV_ATTN_RAWMMA
+  if (false)
+#endif
   for (int j = 0; j < nblk; ++j) {
     if (lane == 0 && w == 0) TRACE(x * 3 + 0, clock64());  // softmax: start waiting S
     tc::mbar_wait(&sm.s_full[x], j & 1);
@@ -300,10 +303,21 @@ __global__ void __launch_bounds__(384, 1)
         tc::tma_load_3d(sm.q[1], &tm_q, &sm.q_full, 0, g * G, tB);
         tc::tma_load_3d(sm.q[1] + kPanel, &tm_q, &sm.q_full, 64, g * G, tB);
       }
+#ifdef IFKV_ATTN_RAWMMA
+      if (false)
+#endif
       for (int j = 0; j < nblk; ++j) {
         const int s = j & 1;
         const uint32_t ph = (j >> 1) & 1;
         tc::mbar_wait(&sm.k_empty[s], ph ^ 1);
+#ifdef IFKV_ATTN_NOTMA_STEADY  // experiment: only the first two K/V blocks are loaded (stale data after)
+        if (j >= 2) {
+          tc::mbar_arrive(&sm.k_full[s]);
+          tc::mbar_wait(&sm.v_empty[s], ph ^ 1);
+          tc::mbar_arrive(&sm.v_full[s]);
+          continue;
+        }
+#endif
         tc::mbar_arrive_expect_tx(&sm.k_full[s], kTile);
         tc::tma_load_2d(sm.k[s], &tm_k, &sm.k_full[s], g * kDh, (b0 + j) * kKeys);
         tc::tma_load_2d(sm.k[s] + kPanel, &tm_k, &sm.k_full[s], g * kDh + 64, (b0 + j) * kKeys);
@@ -316,33 +330,75 @@ __global__ void __launch_bounds__(384, 1)
       constexpr uint32_t idesc_qk = tc::idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idesc_pv = tc::idesc_bf16(128, 128, 0, 1);
       tc::mbar_wait(&sm.q_full, 0);
+      // Descriptors: one base per operand buffer, built once; a K-step adds a
+      // compile-time offset to the 14-bit address field (smem < 256 KB, no carry),
+      // keeping the single-thread issue path short (it sits on the P -> PV chain).
+      const uint64_t dq0 = tc::smem_desc_sw128(tc::smem_u32(sm.q[0]), 16, 1024);
+      const uint64_t dq1 = tc::smem_desc_sw128(tc::smem_u32(sm.q[1]), 16, 1024);
+      const uint64_t dk0 = tc::smem_desc_sw128(tc::smem_u32(sm.k[0]), 16, 1024);
+      const uint64_t dk1 = tc::smem_desc_sw128(tc::smem_u32(sm.k[1]), 16, 1024);
+      const uint64_t dv0 = tc::smem_desc_sw128(tc::smem_u32(sm.v[0]), kPanel, 1024);
+      const uint64_t dv1 = tc::smem_desc_sw128(tc::smem_u32(sm.v[1]), kPanel, 1024);
       auto issue_s = [&](int x, int j) {  // S_x(j) = Q_x K_j^T
-        const uint32_t q_addr = tc::smem_u32(sm.q[x]);
-        const uint32_t k_addr = tc::smem_u32(sm.k[j & 1]);
+        const uint64_t qa = x == 0 ? dq0 : dq1, kb = (j & 1) ? dk1 : dk0;
 #pragma unroll
         for (int t = 0; t < kDh / 16; ++t) {
-          uint64_t a = tc::smem_desc_sw128(q_addr + (t >> 2) * kPanel + (t & 3) * 32, 16, 1024);
-          uint64_t b = tc::smem_desc_sw128(k_addr + (t >> 2) * kPanel + (t & 3) * 32, 16, 1024);
-          tc::mma_bf16_ss(tmem + 256 * x, a, b, idesc_qk, t > 0 ? 1u : 0u);
+          const uint64_t step = (uint64_t)((t >> 2) * (kPanel >> 4) + (t & 3) * 2);  // (bytes >> 4)
+          tc::mma_bf16_ss(tmem + 256 * x, qa + step, kb + step, idesc_qk, t > 0 ? 1u : 0u);
         }
         tc::mma_commit(&sm.s_full[x]);
       };
       auto issue_pv = [&](int x, int j) {  // O_x += P_x(j) V_j, P from TMEM, one key half at a time
-        const uint32_t v_addr = tc::smem_u32(sm.v[j & 1]);
+        const uint64_t vb = (j & 1) ? dv1 : dv0;
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
+#ifndef IFKV_ATTN_ONEPWAIT
           if (hf == 1) {
             tc::mbar_wait(&sm.p_full[x][1], j & 1);
             tc::tc_fence_after();
           }
+#endif
 #pragma unroll
-          for (int t = 4 * hf; t < 4 * hf + 4; ++t) {
+          for (int t = 4 * hf; t < 4 * hf + 4; ++t)
+            tc::mma_bf16_ts(tmem + 256 * x + 128, tmem + 256 * x + 8 * t, vb + (uint64_t)(t * (2048 >> 4)), idesc_pv,
+                            (j > 0 || t > 0) ? 1u : 0u);
+        }
+        if (j == (x == 0 ? nA : nB) - 1) tc::mma_commit(&sm.o_final[x]);
+      };
+#ifdef IFKV_ATTN_RAWMMA  // experiment: the MMA stream alone, no waits (garbage operands)
+      for (int j = 0; j < nblk; ++j) {
+        for (int x = 0; x < 2; ++x) {
+          const uint32_t q_addr = tc::smem_u32(sm.q[x]);
+          const uint32_t k_addr = tc::smem_u32(sm.k[j & 1]);
+#pragma unroll
+          for (int t = 0; t < kDh / 16; ++t) {
+            uint64_t a = tc::smem_desc_sw128(q_addr + (t >> 2) * kPanel + (t & 3) * 32, 16, 1024);
+            uint64_t b = tc::smem_desc_sw128(k_addr + (t >> 2) * kPanel + (t & 3) * 32, 16, 1024);
+            tc::mma_bf16_ss(tmem + 256 * x, a, b, idesc_qk, t > 0 ? 1u : 0u);
+          }
+#ifdef IFKV_ATTN_RAWCOMMIT  // ... with the real kernel's commit cadence
+          tc::mma_commit(&sm.s_full[x]);
+#endif
+        }
+        for (int x = 0; x < 2; ++x) {
+          const uint32_t v_addr = tc::smem_u32(sm.v[j & 1]);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
             uint64_t b = tc::smem_desc_sw128(v_addr + t * 2048, kPanel, 1024);
             tc::mma_bf16_ts(tmem + 256 * x + 128, tmem + 256 * x + 8 * t, b, idesc_pv, (j > 0 || t > 0) ? 1u : 0u);
           }
         }
-        if (j == (x == 0 ? nA : nB) - 1) tc::mma_commit(&sm.o_final[x]);
-      };
+#ifdef IFKV_ATTN_RAWCOMMIT
+        tc::mma_commit(&sm.v_empty[j & 1]);
+        tc::mma_commit(&sm.k_empty[j & 1]);
+#endif
+      }
+      tc::mma_commit(&sm.o_final[0]);
+      tc::mma_commit(&sm.o_final[1]);
+      if (false) {
+#else
+      {
+#endif
       // prologue: S_A(0), S_B(0).  A pair with no visible key at all (every
       // horizon -1: queries of other ranks' chunks in the sharded partial
       // mode) has nblk = 0 and no K block is ever loaded.
@@ -362,7 +418,11 @@ __global__ void __launch_bounds__(384, 1)
           const int nx = x == 0 ? nA : nB;
           if (j >= nx) continue;
           TRACE(6, clock64());  // MMA: start waiting P_x
+#ifdef IFKV_ATTN_ONEPWAIT  // experiment: one P wait per tile-block (the second half's)
+          tc::mbar_wait(&sm.p_full[x][1], j & 1);
+#else
           tc::mbar_wait(&sm.p_full[x][0], j & 1);
+#endif
           TRACE(7, clock64());  // MMA: P_x ready
           if (!v_ready) {
             TRACE(8, clock64());  // MMA: start waiting V
@@ -385,6 +445,7 @@ __global__ void __launch_bounds__(384, 1)
         }
         tc::mma_commit(&sm.v_empty[s]);
         if (next_k) tc::mma_commit(&sm.k_empty[(j + 1) & 1]);
+      }
       }
     }
   } else {

@@ -36,6 +36,13 @@ constexpr float kRescaleLog2 = 8.0f;
 #define IFKV_ATTN4_STAGES 2
 #endif
 constexpr int kStages = IFKV_ATTN4_STAGES;
+// S buffers in TMEM (128 columns each) + O (128 columns): 3 buffers let S(j+3)
+// follow PV(j), so the softmax of block j+1 never waits on the PV(j) handshake.
+#ifndef IFKV_ATTN4_SBUF
+#define IFKV_ATTN4_SBUF 3
+#endif
+constexpr int kSBuf = IFKV_ATTN4_SBUF;
+constexpr uint32_t kColO = 128 * kSBuf;
 
 struct Smem {
   uint8_t q[kTile];
@@ -43,7 +50,8 @@ struct Smem {
   uint8_t v[kStages][kTile];
   uint64_t q_full;
   uint64_t k_full[kStages], k_empty[kStages], v_full[kStages], v_empty[kStages];
-  uint64_t s_full[2], p_full[2][2], pv_done, o_final;  // p_full[S buffer][column half]
+  // p_full[S buffer][column half]; pv_done[i & 1] completes once per PV(i) of that parity
+  uint64_t s_full[kSBuf], p_full[kSBuf][2], pv_done[2], o_final;
   uint32_t tmem_base;
   int n_blocks;
   // row-max exchange [buffer][column half][row]; double-buffered by block
@@ -73,14 +81,19 @@ __device__ __forceinline__ void softmax_half(Smem& sm, uint32_t tmem, int hf, in
   const bool valid = row < (kRows / G) * G && tok < S;
   const int hz = valid ? (int)horizon[tok] : 0;
   const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-  const uint32_t t_o = tmem + 256 + lane_off + 64 * hf;
+  const uint32_t t_o = tmem + kColO + lane_off + 64 * hf;
   const int bar_id = 1 + q;
   float m_used = -INFINITY, l = 0.f;
   for (int j = 0; j < nblk; ++j) {
-    const int b = j & 1;
+    const int b = j % kSBuf, xb = j & 1;  // S buffer, exchange parity
     const uint32_t t_s = tmem + 128 * b + lane_off + 64 * hf;
-    tc::mbar_wait(&sm.s_full[b], (j >> 1) & 1);
+    tc::mbar_wait(&sm.s_full[b], (j / kSBuf) & 1);
     tc::tc_fence_after();
+#ifdef IFKV_ATTN_NOSOFTMAX  // experiment: MMA / TMA pipeline alone
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(&sm.p_full[b][hf]);
+    continue;
+#endif
     const int j0 = (b0 + j) * kKeys + 64 * hf;  // absolute first key of this half
     const bool masked = __any_sync(0xffffffffu, j0 + 63 > hz);
     float v[64];
@@ -105,9 +118,9 @@ __device__ __forceinline__ void softmax_half(Smem& sm, uint32_t tmem, int hf, in
     }
     float mx = fmaxf(m2[0], m2[1]);
     constexpr int kXb = kStages >= 3 ? 1 : 2;
-    sm.xmax[b % kXb][hf][row] = mx;
+    sm.xmax[xb % kXb][hf][row] = mx;
     pair_sync(bar_id);
-    mx = fmaxf(mx, sm.xmax[b % kXb][hf ^ 1][row]);
+    mx = fmaxf(mx, sm.xmax[xb % kXb][hf ^ 1][row]);
     if (kXb == 1) pair_sync(bar_id);  // partner has read before the next block overwrites
     float alpha = 1.f;
     bool need = false;
@@ -118,8 +131,10 @@ __device__ __forceinline__ void softmax_half(Smem& sm, uint32_t tmem, int hf, in
     }
     const float mb = m_used == -INFINITY ? 0.f : m_used * scale_log2;
     if (j > 0 && __any_sync(0xffffffffu, need)) {
-      // O = PV(0..j-1): PV(j-2) completed before S(j) (issue order); wait for PV(j-1)
-      tc::mbar_wait(&sm.pv_done, (j - 1) & 1);
+      // O = PV(0..j-1): wait for PV(j-1) on the barrier of its parity.  PV(j-3)
+      // is complete (S(j) was issued after it) and PV(j+1) cannot be (it needs
+      // P(j+1)), so that barrier is on phase (j-1)/2 or just past it.
+      tc::mbar_wait(&sm.pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
       tc::tc_fence_after();
       const float a = need ? alpha : 1.f;
 #pragma unroll 1
@@ -214,12 +229,13 @@ __global__ void __launch_bounds__(384, 1)
       tc::mbar_init(&sm.v_full[i], 1);
       tc::mbar_init(&sm.v_empty[i], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kSBuf; ++b) {
       tc::mbar_init(&sm.s_full[b], 1);
       tc::mbar_init(&sm.p_full[b][0], 4);  // one elected arrival per softmax warp of the half
       tc::mbar_init(&sm.p_full[b][1], 4);
     }
-    tc::mbar_init(&sm.pv_done, 1);
+    tc::mbar_init(&sm.pv_done[0], 1);
+    tc::mbar_init(&sm.pv_done[1], 1);
     tc::mbar_init(&sm.o_final, 1);
     tc::fence_barrier_init();
   }
@@ -262,7 +278,7 @@ __global__ void __launch_bounds__(384, 1)
       constexpr uint32_t idesc_pv = tc::idesc_bf16(128, 128, 0, 1);
       tc::mbar_wait(&sm.q_full, 0);
       const uint32_t q_addr = tc::smem_u32(sm.q);
-      auto issue_s = [&](int j) {  // S(j) = Q K_j^T into buffer j & 1
+      auto issue_s = [&](int j) {  // S(j) = Q K_j^T into buffer j % kSBuf
         const int s = j % kStages;
         tc::mbar_wait(&sm.k_full[s], (j / kStages) & 1);
         tc::tc_fence_after();
@@ -271,32 +287,32 @@ __global__ void __launch_bounds__(384, 1)
         for (int t = 0; t < kDh / 16; ++t) {
           uint64_t a = tc::smem_desc_sw128(q_addr + (t >> 2) * kPanel + (t & 3) * 32, 16, 1024);
           uint64_t b = tc::smem_desc_sw128(k_addr + (t >> 2) * kPanel + (t & 3) * 32, 16, 1024);
-          tc::mma_bf16_ss(tmem + 128 * (j & 1), a, b, idesc_qk, t > 0 ? 1u : 0u);
+          tc::mma_bf16_ss(tmem + 128 * (j % kSBuf), a, b, idesc_qk, t > 0 ? 1u : 0u);
         }
-        tc::mma_commit(&sm.s_full[j & 1]);
+        tc::mma_commit(&sm.s_full[j % kSBuf]);
         tc::mma_commit(&sm.k_empty[s]);
       };
       issue_s(0);
-      if (nblk > 1) issue_s(1);
+      for (int j = 1; j < kSBuf && j < nblk; ++j) issue_s(j);
       for (int j = 0; j < nblk; ++j) {
-        const int b = j & 1, s = j % kStages;
+        const int b = j % kSBuf, s = j % kStages;
         const uint32_t v_addr = tc::smem_u32(sm.v[s]);
         tc::mbar_wait(&sm.v_full[s], (j / kStages) & 1);
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {  // keys [64 hf, 64 hf + 64): P at buffer cols [64 hf, 64 hf + 32)
-          tc::mbar_wait(&sm.p_full[b][hf], (j >> 1) & 1);
+          tc::mbar_wait(&sm.p_full[b][hf], (j / kSBuf) & 1);
           tc::tc_fence_after();
 #pragma unroll
           for (int t = 4 * hf; t < 4 * hf + 4; ++t) {
             uint64_t bd = tc::smem_desc_sw128(v_addr + t * 2048, kPanel, 1024);
-            tc::mma_bf16_ts(tmem + 256, tmem + 128 * b + 64 * hf + 8 * (t - 4 * hf), bd, idesc_pv,
+            tc::mma_bf16_ts(tmem + kColO, tmem + 128 * b + 64 * hf + 8 * (t - 4 * hf), bd, idesc_pv,
                             (j > 0 || t > 0) ? 1u : 0u);
           }
         }
-        tc::mma_commit(&sm.pv_done);
+        tc::mma_commit(&sm.pv_done[j & 1]);
         tc::mma_commit(&sm.v_empty[s]);
         if (j == nblk - 1) tc::mma_commit(&sm.o_final);
-        if (j + 2 < nblk) issue_s(j + 2);  // buffer b again: PV(j) has read P(j) (in-order pipe)
+        if (j + kSBuf < nblk) issue_s(j + kSBuf);  // buffer b again: PV(j) has read P(j) (in-order pipe)
       }
     }
   } else if (t0 < S) {
