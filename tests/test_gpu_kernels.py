@@ -200,3 +200,38 @@ def test_recompute_attention_unsorted_and_empty_horizons(T, cuda, partial, n_emp
     want, _ = O.prefix_attention(q.double().cpu().numpy()[rows], k.double().cpu().numpy(), v.double().cpu().numpy(),
                                  hz[rows])
     assert np.max(np.abs(got - want)) <= 1e-2 * np.max(np.abs(want))
+
+
+@pytest.mark.parametrize("partial", [False, True])
+def test_recompute_attention_large_grid_v2_path(T, cuda, partial):
+    """A grid of >= two waves (k = 2600 at 32 q / 8 kv heads) runs the two-tile
+    ping-pong kernel (small grids run v4): compare with the SIMT kernel on every
+    row and with the oracle on sampled rows."""
+    from paper_2603_05353_b200 import engine as E
+
+    rng = np.random.default_rng(5)
+    hkv, dh, n, H, k = 8, 128, 6000, 32, 2600
+    hz = np.sort(rng.choice(n, k, replace=False))
+    if partial:
+        hz[:70] = -1  # keyless rows (and one keyless tile pair) of the sharded partial mode
+    q = T.as_tensor(rng.standard_normal((k, H, dh)), dtype=T.float32).to(cuda, T.bfloat16)
+    kk = T.as_tensor(rng.standard_normal((n, hkv, dh)), dtype=T.float32).to(cuda, T.bfloat16)
+    vv = T.as_tensor(rng.standard_normal((n, hkv, dh)), dtype=T.float32).to(cuda, T.bfloat16)
+    hzt = T.as_tensor(hz, device=cuda)
+    if partial:
+        tc, ml = E.recompute_attn_partial(q, kk, vv, hzt, H, hkv, dh)
+        assert np.all(ml[:70].cpu().numpy()[..., 1] == 0)
+    else:
+        tc = E.recompute_attn(q, kk, vv, hzt, H, hkv, dh)
+    simt = E.recompute_attn(q, kk, vv, hzt, H, hkv, dh, impl="simt") if not partial else None
+    got = tc.double().cpu().numpy()
+    rows = np.arange(70 if partial else 0, k)
+    if simt is not None:
+        ref = simt.double().cpu().numpy()
+        assert np.max(np.abs(got - ref)) <= 1e-2 * np.max(np.abs(ref))
+    pick = rows[rng.choice(rows.size, 40, replace=False)]
+    want, _ = O.prefix_attention(q.double().cpu().numpy()[pick], kk.double().cpu().numpy(),
+                                 vv.double().cpu().numpy(), hz[pick])
+    assert np.max(np.abs(got[pick] - want)) <= 1e-2 * np.max(np.abs(want))
+    if partial:
+        assert np.all(got[:70] == 0)
