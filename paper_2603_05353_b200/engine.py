@@ -348,18 +348,20 @@ def _plan_items(groups: Sequence[PromptGroup], M: int, item_keys: int = ITEM_KEY
 
 def _tc_item_keys(groups, Hkv: int, G: int, M: int, sms: int = 148) -> int:
     """Keys per tensor-core work item: the longest multiple of 128 (<= 16
-    blocks) that still gives >= 2 CTAs per SM; fewer, longer items mean fewer
-    (m, l, O) partials to write and merge."""
+    blocks) that still keeps >= 80 % of the SMs busy (one 224 KB CTA per SM).
+    Long items amortise each CTA's setup (TMEM alloc, 96 KB of split queries)
+    and leave fewer (m, l, O) partials to merge: at C2, 2048-key items take
+    the scoring stage from 5.9 to 5.3-5.7 ms vs 512-key items (2 CTAs per SM)."""
+    if os.environ.get("IFKV_PROMPT_ITEM_KEYS"):  # A/B override (multiple of 128)
+        return int(os.environ["IFKV_PROMPT_ITEM_KEYS"])
     hpt = max(1, min(128 // M, G))
     chunks = Hkv * (-(-G // hpt))
     runs = [n for g in groups for (_, n, _) in g.segments]
-    best = 128
-    for ipc in (2, 4, 8, 16):
+    for ipc in (16, 8, 4, 2):
         ctas = chunks * sum(-(-n // (128 * ipc)) for n in runs)
-        if ctas < 2 * sms:
-            break
-        best = 128 * ipc
-    return best
+        if ctas >= 0.8 * sms:
+            return 128 * ipc
+    return 128
 
 
 def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], capture_layer: Optional[int] = None,
