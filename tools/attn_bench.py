@@ -22,7 +22,8 @@ def run(lib, iters=30):
     from paper_2603_05353_b200 import engine as E
 
     rng = np.random.default_rng(0)
-    n, k, H, Hkv, Dh = 32768, int(os.environ.get("ATTN_K", "4916")), 32, 8, 128
+    n, k, Dh = int(os.environ.get("ATTN_N", "32768")), int(os.environ.get("ATTN_K", "4916")), 128
+    H, Hkv = int(os.environ.get("ATTN_H", "32")), int(os.environ.get("ATTN_HKV", "8"))
     sel = np.sort(rng.choice(n, k, replace=False))
     q = torch.randn(k, H, Dh, device="cuda", dtype=torch.bfloat16)
     kk = torch.randn(n, Hkv, Dh, device="cuda", dtype=torch.bfloat16)
