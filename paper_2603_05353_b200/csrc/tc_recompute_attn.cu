@@ -68,13 +68,20 @@ __device__ int g_attn_trace_n[12];
 #define IFKV_ATTN_POLY_MASK 0x00
 #endif
 
+// P published in kPParts key parts per block (2: halves; 4: quarters, A/B):
+// the PV MMA of a part starts while the next part is exponentiated.
+#ifndef IFKV_ATTN_PPARTS
+#define IFKV_ATTN_PPARTS 2
+#endif
+constexpr int kPParts = IFKV_ATTN_PPARTS;
+
 struct Smem {
   uint8_t q[2][kTile];
   uint8_t k[2][kTile];
   uint8_t v[2][kTile];
   uint64_t q_full;
   uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
-  uint64_t s_full[2], p_full[2][2], o_final[2];  // p_full[tile][key half]
+  uint64_t s_full[2], p_full[2][kPParts], o_final[2];  // p_full[tile][key part]
   uint32_t tmem_base;
   int n_blocks[2];
 };
@@ -115,8 +122,7 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
     if (lane == 0 && w == 0) TRACE(x * 3 + 1, clock64());  // softmax: S ready
 #ifdef IFKV_ATTN_NOSOFTMAX  // experiment: pure MMA / TMA pipeline throughput
     tc::tc_fence_before();
-    tc::mbar_arrive(&sm.p_full[x][0]);
-    tc::mbar_arrive(&sm.p_full[x][1]);
+    for (int q = 0; q < kPParts; ++q) tc::mbar_arrive(&sm.p_full[x][q]);
     if (lane == 0 && w == 0) TRACE(x * 3 + 2, clock64());
     continue;
 #endif
@@ -176,6 +182,12 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
       float2 sum2 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int c = 0; c < 64; c += 2) {
+        if (kPParts == 4 && c == 32) {  // publish the first quarter of this half
+          tc::tmem_st16(t_s + hf * 32, pk);
+          tc::tmem_st_wait();
+          tc::tc_fence_before();
+          tc::mbar_arrive(&sm.p_full[x][2 * hf]);
+        }
         // packed x = s * scale - m; exp2 on the MUFU, or on the FMA pipe for
         // the pairs selected by IFKV_ATTN_POLY_MASK in unmasked blocks
         // (ex2.approx.ftz(-inf) = +0 on the masked ones)
@@ -190,13 +202,13 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
         pk[c / 2] = tc::pack_bf16(e.x, e.y);
       }
       sum += sum2.x + sum2.y;
-      tc::tmem_st16(t_s + hf * 32, pk);
+      if (kPParts == 2) tc::tmem_st16(t_s + hf * 32, pk);
       tc::tmem_st16(t_s + hf * 32 + 16, pk + 16);
       // publish this half of P: the PV MMA over keys [64 hf, 64 hf + 64)
       // starts while the next half is still being exponentiated
       tc::tmem_st_wait();
       tc::tc_fence_before();
-      tc::mbar_arrive(&sm.p_full[x][hf]);
+      tc::mbar_arrive(&sm.p_full[x][kPParts == 4 ? 2 * hf + 1 : hf]);
     }
     l = l * alpha + sum;
     if (lane == 0 && w == 0) TRACE(x * 3 + 2, clock64());  // softmax: P published
@@ -267,8 +279,7 @@ __global__ void __launch_bounds__(384, 1)
       tc::mbar_init(&sm.v_full[i], 1);
       tc::mbar_init(&sm.v_empty[i], 1);
       tc::mbar_init(&sm.s_full[i], 1);
-      tc::mbar_init(&sm.p_full[i][0], 128);
-      tc::mbar_init(&sm.p_full[i][1], 128);
+      for (int q = 0; q < kPParts; ++q) tc::mbar_init(&sm.p_full[i][q], 128);
       tc::mbar_init(&sm.o_final[i], 1);
     }
     tc::fence_barrier_init();
@@ -351,15 +362,16 @@ __global__ void __launch_bounds__(384, 1)
       auto issue_pv = [&](int x, int j) {  // O_x += P_x(j) V_j, P from TMEM, one key half at a time
         const uint64_t vb = (j & 1) ? dv1 : dv0;
 #pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
+        for (int hf = 0; hf < kPParts; ++hf) {
 #ifndef IFKV_ATTN_ONEPWAIT
-          if (hf == 1) {
-            tc::mbar_wait(&sm.p_full[x][1], j & 1);
+          if (hf > 0) {
+            tc::mbar_wait(&sm.p_full[x][hf], j & 1);
             tc::tc_fence_after();
           }
 #endif
+          constexpr int kT = 8 / kPParts;  // K-steps (16 keys) per part
 #pragma unroll
-          for (int t = 4 * hf; t < 4 * hf + 4; ++t)
+          for (int t = kT * hf; t < kT * hf + kT; ++t)
             tc::mma_bf16_ts(tmem + 256 * x + 128, tmem + 256 * x + 8 * t, vb + (uint64_t)(t * (2048 >> 4)), idesc_pv,
                             (j > 0 || t > 0) ? 1u : 0u);
         }
@@ -418,8 +430,8 @@ __global__ void __launch_bounds__(384, 1)
           const int nx = x == 0 ? nA : nB;
           if (j >= nx) continue;
           TRACE(6, clock64());  // MMA: start waiting P_x
-#ifdef IFKV_ATTN_ONEPWAIT  // experiment: one P wait per tile-block (the second half's)
-          tc::mbar_wait(&sm.p_full[x][1], j & 1);
+#ifdef IFKV_ATTN_ONEPWAIT  // experiment: one P wait per tile-block (the last part's)
+          tc::mbar_wait(&sm.p_full[x][kPParts - 1], j & 1);
 #else
           tc::mbar_wait(&sm.p_full[x][0], j & 1);
 #endif
