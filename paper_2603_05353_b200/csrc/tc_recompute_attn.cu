@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(384, 1)
         tc::tma_load_2d(sm.v[s], &tm_v, &sm.v_full[s], g * kDh, (b0 + j) * kKeys);
         tc::tma_load_2d(sm.v[s] + kPanel, &tm_v, &sm.v_full[s], g * kDh + 64, (b0 + j) * kKeys);
       }
-    } else if (warp == 1 && lane == 0) {
+    } else if (warp == 1) {  // MMA issuer: the whole warp runs this, one elected lane issues (tc::*_ws)
       constexpr uint32_t idesc_qk = tc::idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idesc_pv = tc::idesc_bf16(128, 128, 0, 1);
       tc::mbar_wait(&sm.q_full, 0);
@@ -355,9 +355,9 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int t = 0; t < kDh / 16; ++t) {
           const uint64_t step = (uint64_t)((t >> 2) * (kPanel >> 4) + (t & 3) * 2);  // (bytes >> 4)
-          tc::mma_bf16_ss(tmem + 256 * x, qa + step, kb + step, idesc_qk, t > 0 ? 1u : 0u);
+          tc::mma_bf16_ss_ws(tmem + 256 * x, qa + step, kb + step, idesc_qk, t > 0 ? 1u : 0u);
         }
-        tc::mma_commit(&sm.s_full[x]);
+        tc::mma_commit_ws(&sm.s_full[x]);
       };
       auto issue_pv = [&](int x, int j) {  // O_x += P_x(j) V_j, P from TMEM, one key half at a time
         const uint64_t vb = (j & 1) ? dv1 : dv0;
@@ -372,10 +372,10 @@ __global__ void __launch_bounds__(384, 1)
           constexpr int kT = 8 / kPParts;  // K-steps (16 keys) per part
 #pragma unroll
           for (int t = kT * hf; t < kT * hf + kT; ++t)
-            tc::mma_bf16_ts(tmem + 256 * x + 128, tmem + 256 * x + 8 * t, vb + (uint64_t)(t * (2048 >> 4)), idesc_pv,
+            tc::mma_bf16_ts_ws(tmem + 256 * x + 128, tmem + 256 * x + 8 * t, vb + (uint64_t)(t * (2048 >> 4)), idesc_pv,
                             (j > 0 || t > 0) ? 1u : 0u);
         }
-        if (j == (x == 0 ? nA : nB) - 1) tc::mma_commit(&sm.o_final[x]);
+        if (j == (x == 0 ? nA : nB) - 1) tc::mma_commit_ws(&sm.o_final[x]);
       };
 #ifdef IFKV_ATTN_RAWMMA  // experiment: the MMA stream alone, no waits (garbage operands)
       for (int j = 0; j < nblk; ++j) {
@@ -386,10 +386,10 @@ __global__ void __launch_bounds__(384, 1)
           for (int t = 0; t < kDh / 16; ++t) {
             uint64_t a = tc::smem_desc_sw128(q_addr + (t >> 2) * kPanel + (t & 3) * 32, 16, 1024);
             uint64_t b = tc::smem_desc_sw128(k_addr + (t >> 2) * kPanel + (t & 3) * 32, 16, 1024);
-            tc::mma_bf16_ss(tmem + 256 * x, a, b, idesc_qk, t > 0 ? 1u : 0u);
+            tc::mma_bf16_ss_ws(tmem + 256 * x, a, b, idesc_qk, t > 0 ? 1u : 0u);
           }
 #ifdef IFKV_ATTN_RAWCOMMIT  // ... with the real kernel's commit cadence
-          tc::mma_commit(&sm.s_full[x]);
+          tc::mma_commit_ws(&sm.s_full[x]);
 #endif
         }
         for (int x = 0; x < 2; ++x) {
@@ -397,16 +397,16 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
           for (int t = 0; t < 8; ++t) {
             uint64_t b = tc::smem_desc_sw128(v_addr + t * 2048, kPanel, 1024);
-            tc::mma_bf16_ts(tmem + 256 * x + 128, tmem + 256 * x + 8 * t, b, idesc_pv, (j > 0 || t > 0) ? 1u : 0u);
+            tc::mma_bf16_ts_ws(tmem + 256 * x + 128, tmem + 256 * x + 8 * t, b, idesc_pv, (j > 0 || t > 0) ? 1u : 0u);
           }
         }
 #ifdef IFKV_ATTN_RAWCOMMIT
-        tc::mma_commit(&sm.v_empty[j & 1]);
-        tc::mma_commit(&sm.k_empty[j & 1]);
+        tc::mma_commit_ws(&sm.v_empty[j & 1]);
+        tc::mma_commit_ws(&sm.k_empty[j & 1]);
 #endif
       }
-      tc::mma_commit(&sm.o_final[0]);
-      tc::mma_commit(&sm.o_final[1]);
+      tc::mma_commit_ws(&sm.o_final[0]);
+      tc::mma_commit_ws(&sm.o_final[1]);
       if (false) {
 #else
       {
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(384, 1)
         tc::tc_fence_after();
         for (int x = 0; x < 2; ++x)
           if ((x == 0 ? nA : nB) > 0) issue_s(x, 0);
-        tc::mma_commit(&sm.k_empty[0]);  // K_0 is only read by the prologue
+        tc::mma_commit_ws(&sm.k_empty[0]);  // K_0 is only read by the prologue
       }
       for (int j = 0; j < nblk; ++j) {
         const int s = j & 1;
@@ -429,34 +429,34 @@ __global__ void __launch_bounds__(384, 1)
         for (int x = 0; x < 2; ++x) {
           const int nx = x == 0 ? nA : nB;
           if (j >= nx) continue;
-          TRACE(6, clock64());  // MMA: start waiting P_x
+          if (lane == 0) TRACE(6, clock64());  // MMA: start waiting P_x
 #ifdef IFKV_ATTN_ONEPWAIT  // experiment: one P wait per tile-block (the last part's)
           tc::mbar_wait(&sm.p_full[x][kPParts - 1], j & 1);
 #else
           tc::mbar_wait(&sm.p_full[x][0], j & 1);
 #endif
-          TRACE(7, clock64());  // MMA: P_x ready
+          if (lane == 0) TRACE(7, clock64());  // MMA: P_x ready
           if (!v_ready) {
-            TRACE(8, clock64());  // MMA: start waiting V
+            if (lane == 0) TRACE(8, clock64());  // MMA: start waiting V
             tc::mbar_wait(&sm.v_full[s], ph);
-            TRACE(9, clock64());
+            if (lane == 0) TRACE(9, clock64());
             v_ready = true;
           }
           tc::tc_fence_after();
           issue_pv(x, j);
           if (j + 1 < nx) {
             if (!next_k) {
-              TRACE(10, clock64());  // MMA: start waiting K
+              if (lane == 0) TRACE(10, clock64());  // MMA: start waiting K
               tc::mbar_wait(&sm.k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
-              TRACE(11, clock64());
+              if (lane == 0) TRACE(11, clock64());
               tc::tc_fence_after();
               next_k = true;
             }
             issue_s(x, j + 1);
           }
         }
-        tc::mma_commit(&sm.v_empty[s]);
-        if (next_k) tc::mma_commit(&sm.k_empty[(j + 1) & 1]);
+        tc::mma_commit_ws(&sm.v_empty[s]);
+        if (next_k) tc::mma_commit_ws(&sm.k_empty[(j + 1) & 1]);
       }
       }
     }

@@ -72,10 +72,6 @@ def _s():
     return N.stream_handle()
 
 
-def require_cuda(t, what: str):
-    if not t.is_cuda:
-        raise ConfigurationError(f"{what} must be a CUDA tensor")
-
 
 # ---------------------------------------------------------------------------
 # thin wrappers
