@@ -64,12 +64,13 @@ class Comm:
     def all_gather(self, t) -> list:
         return [t]
 
-    def all_to_all(self, parts: list) -> list:
-        return list(parts)
-
-    def all_gather_var(self, t) -> list:
-        """all_gather for tensors whose first dimension differs per rank."""
+    def all_gather_var(self, t, sizes=None) -> list:
+        """all_gather for tensors whose first dimension differs per rank
+        (``sizes``: the per-rank first dimensions when already known)."""
         return self.all_gather(t)
+
+    def all_to_all(self, parts: list, recv_sizes=None) -> list:
+        return list(parts)
 
 
 class TorchComm(Comm):
@@ -93,15 +94,16 @@ class TorchComm(Comm):
         s = torch.tensor([n], dtype=torch.int64, device=device)
         return [int(x.item()) for x in self.all_gather(s)]
 
-    def all_gather_var(self, t):
+    def all_gather_var(self, t, sizes=None):
         t = t.contiguous()
-        sizes = self._sizes(t.shape[0], t.device)
+        if sizes is None:  # one host round trip; callers in per-layer loops pass known sizes
+            sizes = self._sizes(t.shape[0], t.device)
         cap = max(sizes) if sizes else 0
         pad = t.new_zeros((cap,) + tuple(t.shape[1:]))
         pad[: t.shape[0]] = t
         return [x[:n] for x, n in zip(self.all_gather(pad), sizes)]
 
-    def all_to_all(self, parts):
+    def all_to_all(self, parts, recv_sizes=None):
         parts = [p.contiguous() for p in parts]
         torch = _torch()
         if self.dist.get_backend(self.group) == "gloo":
@@ -109,17 +111,18 @@ class TorchComm(Comm):
             # (and their sizes) and keep the slices addressed to this rank
             sizes = torch.tensor([p.shape[0] for p in parts], dtype=torch.int64, device=parts[0].device)
             all_sizes = [s.tolist() for s in self.all_gather(sizes)]
-            all_flat = self.all_gather_var(torch.cat(parts))
+            all_flat = self.all_gather_var(torch.cat(parts), [sum(x) for x in all_sizes])
             out = []
             for r in range(self.world):
                 off = sum(all_sizes[r][: self.rank])
                 out.append(all_flat[r][off: off + all_sizes[r][self.rank]])
             return out
-        # receive sizes first (first dimension may differ)
-        send_n = torch.tensor([p.shape[0] for p in parts], dtype=torch.int64, device=parts[0].device)
-        recv_n = torch.empty_like(send_n)
-        self.dist.all_to_all_single(recv_n, send_n, group=self.group)
-        recv = [parts[0].new_empty((int(n),) + tuple(parts[0].shape[1:])) for n in recv_n.tolist()]
+        if recv_sizes is None:  # receive sizes first (first dimension may differ)
+            send_n = torch.tensor([p.shape[0] for p in parts], dtype=torch.int64, device=parts[0].device)
+            recv_n = torch.empty_like(send_n)
+            self.dist.all_to_all_single(recv_n, send_n, group=self.group)
+            recv_sizes = recv_n.tolist()
+        recv = [parts[0].new_empty((int(n),) + tuple(parts[0].shape[1:])) for n in recv_sizes]
         self.dist.all_to_all(recv, parts, group=self.group)
         return recv
 
@@ -171,10 +174,10 @@ class ThreadComm(Comm):
     def all_gather(self, t):
         return self._exchange(t, lambda r, x: x if r == self.rank else x.clone())
 
-    def all_gather_var(self, t):
+    def all_gather_var(self, t, sizes=None):
         return self.all_gather(t)
 
-    def all_to_all(self, parts):
+    def all_to_all(self, parts, recv_sizes=None):
         return self._exchange(list(parts), lambda r, x: x[self.rank].clone())
 
 
@@ -329,14 +332,19 @@ def sharded_recompute(weights, shard: Shard, cache: AssembledCache, selected_glo
     to_decode_layout(cache, cfg.rope_base, targets=grows_np)
     ids = cache.token_ids_device().index_select(0, dst)
 
+    # per-rank query counts and the local causal horizons of every rank's
+    # queries are layer-invariant: exchange them once, so the per-layer
+    # collectives below need no host round trip (the GPU never drains)
+    hz_parts = comm.all_gather_var(sel_g)
+    sizes = [int(h.numel()) for h in hz_parts]
+    hz_local = torch.searchsorted(grows, torch.cat(hz_parts), right=True) - 1
+    mine_n = [sizes[comm.rank]] * comm.world
+
     def attn_fn(li, q_local, k_layer, v_layer):
-        q_all = torch.cat(comm.all_gather_var(q_local))
-        hz_parts = comm.all_gather_var(sel_g)
-        sizes = [int(h.numel()) for h in hz_parts]
-        hz_local = torch.searchsorted(grows, torch.cat(hz_parts), right=True) - 1
+        q_all = torch.cat(comm.all_gather_var(q_local, sizes))
         ctx, ml = E.recompute_attn_partial(q_all, k_layer, v_layer, hz_local, H, Hkv, Dh)
-        back_ctx = comm.all_to_all(list(torch.split(ctx, sizes)))
-        back_ml = comm.all_to_all(list(torch.split(ml, sizes)))
+        back_ctx = comm.all_to_all(list(torch.split(ctx, sizes)), mine_n)
+        back_ml = comm.all_to_all(list(torch.split(ml, sizes)), mine_n)
         return merge_query_states(back_ctx, back_ml).to(q_local.dtype)
 
     E.layer_stack(weights, ids, sel_g, cache.keys, cache.values, dst, sel_g, attn_fn=attn_fn)
