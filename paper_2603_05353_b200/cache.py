@@ -228,14 +228,14 @@ def decode_targets(cache: AssembledCache) -> np.ndarray:
     return np.concatenate([np.arange(n, dtype=np.int64), cache.row_positions[n:]])
 
 
-def _delta_table(deltas: np.ndarray, d_head: int, rope_base: float, device):
-    """Row table (int32, -1 for delta 0) and the fp64-derived cos/sin table
-    of the distinct nonzero deltas."""
+def _delta_rows(deltas: np.ndarray):
+    """Host half of the rotation table: per row, the index of its delta among
+    the distinct nonzero deltas (-1 for delta 0), and those deltas."""
     deltas = np.asarray(deltas, dtype=np.int64)
     # runs of constant delta (one per chunk in the usual layouts): O(n), no sort
     cut = np.flatnonzero(np.diff(deltas)) + 1
     starts = np.concatenate([[0], cut])
-    run_d = deltas[starts]
+    run_d = deltas[starts] if deltas.size else deltas
     if np.unique(run_d).size == run_d.size:  # every run has its own delta
         nz = run_d != 0
         rid = np.full(run_d.size, -1, np.int32)
@@ -249,8 +249,15 @@ def _delta_table(deltas: np.ndarray, d_head: int, rope_base: float, device):
         remap[nzu] = np.arange(int(nzu.sum()), dtype=np.int32)
         tab = remap[inv.astype(np.int32)]
         uniq_nz = uniq[nzu]
+    return tab.astype(np.int32), uniq_nz
+
+
+def _delta_table(deltas: np.ndarray, d_head: int, rope_base: float, device):
+    """Row table (int32, -1 for delta 0) and the fp64-derived cos/sin table
+    of the distinct nonzero deltas."""
+    tab, uniq_nz = _delta_rows(deltas)
     cs = E.rope_table(uniq_nz if uniq_nz.size else np.zeros(1, np.int64), d_head, rope_base, device)
-    return E.h2d(tab.astype(np.int32), device), cs
+    return E.h2d(tab, device), cs
 
 
 def decode_view(cache: AssembledCache, rope_base: float):
