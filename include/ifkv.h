@@ -125,11 +125,13 @@ typedef struct {
   int32_t score;    /* 1: context item whose columns are scored             */
 } ifkv_attn_item;
 
-/* Partial softmax state per (item, head, row): ml = (max, sum exp), o = sum p v. */
+/* Partial softmax state per (item, head, row): ml = (max, sum exp), o = sum p v.
+ * max_keys (<= 128) bounds every item's n_keys and sizes the staging smem
+ * (prompt items: M keys -> several CTAs per SM). */
 int ifkv_prompt_attn_partial(int kv_dtype, const float* qd, const void* k_slab, const void* v_slab,
                              const float* k_prompt, const float* v_prompt, const ifkv_attn_item* items,
-                             int n_items, int H, int Hkv, int M, int Dh, float scale, float* part_ml,
-                             float* part_o, void* stream);
+                             int n_items, int max_keys, int H, int Hkv, int M, int Dh, float scale,
+                             float* part_ml, float* part_o, void* stream);
 /* Merge the partials of each group's items in a fixed order -- its context
  * items [item_begin[g], item_begin[g+1]) then, if prompt_item0 >= 0, its
  * prompt item prompt_item0 + g: ctx [G][M][H][Dh] fp32, final ml [G][H][M][2];

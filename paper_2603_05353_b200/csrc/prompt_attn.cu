@@ -48,15 +48,15 @@ __device__ void stage_item(const ifkv_attn_item& it, int kv_dtype, const void* k
 __global__ void __launch_bounds__(256) prompt_attn_partial_kernel(
     int kv_dtype, const float* __restrict__ qd, const void* __restrict__ k_slab, const void* __restrict__ v_slab,
     const float* __restrict__ k_prompt, const float* __restrict__ v_prompt, const ifkv_attn_item* __restrict__ items,
-    int H, int Hkv, int M, int Dh, float scale, float* __restrict__ part_ml, float* __restrict__ part_o) {
+    int kmax, int H, int Hkv, int M, int Dh, float scale, float* __restrict__ part_ml, float* __restrict__ part_o) {
   extern __shared__ float smem[];
   const ifkv_attn_item it = items[blockIdx.x];
   const int g = blockIdx.y;
   const int grp = H / Hkv;
   const int n = it.n_keys;
-  float* Ks = smem;                                  // [n][Dh+1]
-  float* Vs = Ks + kItemKeysMax * (Dh + 1);           // [n][Dh]
-  float* Qs = Vs + kItemKeysMax * Dh;                 // [8][Dh]
+  float* Ks = smem;                  // [n][Dh+1]
+  float* Vs = Ks + kmax * (Dh + 1);  // [n][Dh]
+  float* Qs = Vs + kmax * Dh;        // [8][Dh]
   stage_item(it, kv_dtype, k_slab, v_slab, k_prompt, v_prompt, M, Hkv, Dh, g, Ks, Vs);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -238,17 +238,18 @@ __global__ void __launch_bounds__(128) score_columns_kernel(int kv_dtype, const 
 
 using namespace ifkv;
 
-static size_t partial_smem(int Dh) { return (size_t)(kItemKeysMax * (Dh + 1) + kItemKeysMax * Dh + 8 * Dh) * 4; }
+static size_t partial_smem(int Dh, int kmax) { return (size_t)(kmax * (Dh + 1) + kmax * Dh + 8 * Dh) * 4; }
 static size_t score_smem(int Dh, int M) { return (size_t)(kItemKeysMax * (Dh + 1) + M * Dh) * 4; }
 
 extern "C" int ifkv_prompt_attn_partial(int kv_dtype, const float* qd, const void* k_slab, const void* v_slab,
                                         const float* k_prompt, const float* v_prompt, const ifkv_attn_item* items,
-                                        int n_items, int H, int Hkv, int M, int Dh, float scale, float* part_ml,
-                                        float* part_o, void* stream) {
+                                        int n_items, int max_keys, int H, int Hkv, int M, int Dh, float scale,
+                                        float* part_ml, float* part_o, void* stream) {
   IFKV_CHECK_ARG(kv_dtype == IFKV_F32 || kv_dtype == IFKV_BF16, "prompt_attn_partial: bad dtype");
   IFKV_CHECK_ARG(Dh % 2 == 0 && Dh <= 256 && H % Hkv == 0 && M > 0, "prompt_attn_partial: bad shape");
+  IFKV_CHECK_ARG(max_keys >= 1 && max_keys <= kItemKeysMax, "prompt_attn_partial: max_keys must be in [1, 128]");
   if (n_items <= 0) return IFKV_OK;
-  size_t sm = partial_smem(Dh);
+  size_t sm = partial_smem(Dh, max_keys);
   IFKV_CUDA_CALL(cudaFuncSetAttribute(prompt_attn_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)sm),
                  "prompt_attn_partial: smem attribute");
@@ -258,8 +259,8 @@ extern "C" int ifkv_prompt_attn_partial(int kv_dtype, const float* qd, const voi
   while (splits > 1 && ctas * splits > 4 * 148) splits = (splits + 1) / 2;  // enough CTAs, bounded restaging
   dim3 grid(n_items, Hkv, splits);
   prompt_attn_partial_kernel<<<grid, 256, sm, as_stream(stream)>>>(kv_dtype, qd, k_slab, v_slab, k_prompt,
-                                                                     v_prompt, items, H, Hkv, M, Dh, scale, part_ml,
-                                                                     part_o);
+                                                                     v_prompt, items, max_keys, H, Hkv, M, Dh, scale,
+                                                                     part_ml, part_o);
   IFKV_LAUNCH_CHECK("prompt_attn_partial");
   return IFKV_OK;
 }

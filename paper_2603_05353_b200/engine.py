@@ -430,10 +430,11 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
                        n_rows, items_p, n_ctx, item_keys, H, Hkv, M, scale, N.ptr(part_ml), N.ptr(part_o), _s())
             elif n_ctx:
                 N.call("ifkv_prompt_attn_partial", kv_dt, N.ptr(qd), N.ptr(slab_k[li]), N.ptr(slab_v[li]), N.ptr(kp),
-                       N.ptr(vp), items_p, n_ctx, H, Hkv, M, Dh, scale, N.ptr(part_ml), N.ptr(part_o), _s())
+                       N.ptr(vp), items_p, n_ctx, item_keys, H, Hkv, M, Dh, scale, N.ptr(part_ml), N.ptr(part_o),
+                       _s())
             if include_prompt:
                 N.call("ifkv_prompt_attn_partial", kv_dt, N.ptr(qd), N.ptr(slab_k[li]), N.ptr(slab_v[li]), N.ptr(kp),
-                       N.ptr(vp), prompt_items_p, n_items - n_ctx, H, Hkv, M, Dh, scale,
+                       N.ptr(vp), prompt_items_p, n_items - n_ctx, M, H, Hkv, M, Dh, scale,
                        part_ml.data_ptr() + n_ctx * stride_ml, part_o.data_ptr() + n_ctx * stride_o, _s())
             fuse_split = bf16 and merge_hook is None and not capture
             N.call("ifkv_prompt_attn_merge", N.ptr(part_ml), N.ptr(part_o), ib_p, n_ctx if include_prompt else -1, G,
