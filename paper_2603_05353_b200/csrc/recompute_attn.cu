@@ -111,10 +111,14 @@ extern "C" int ifkv_recompute_attn_tc(const void* q, const void* k_layer, const 
 extern "C" int ifkv_recompute_attn_tc_v4(const void* q, const void* k_layer, const void* v_layer,
                                          const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows,
                                          float scale, void* out, float* ml_out, void* stream);
-// tcgen05 kernel generation: v2 (two ping-ponging tiles per CTA) while its
-// grid fills two waves of the GPU and G divides 128, else v4 (one tile per CTA, double-buffered
+extern "C" int ifkv_recompute_attn_tc_v5(const void* q, const void* k_layer, const void* v_layer,
+                                         const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows,
+                                         float scale, void* out, float* ml_out, void* stream);
+// tcgen05 kernel generation: v5 (two ping-ponging tiles per CTA, P staged in
+// smem so S(j+1) follows the read of S(j); 3-5 % faster than v2, identical
+// results) while the grid fills two waves of the GPU and G divides 128, else v4 (one tile per CTA, double-buffered
 // S, column-split softmax: twice the CTAs; measured 0.474 vs 0.574 ms at
-// k = 1639, 0.650 vs 0.624 ms at k = 2458).  IFKV_ATTN_GEN=2/4 pins one (A/B).
+// k = 1639, 0.650 vs 0.624 ms at k = 2458).  IFKV_ATTN_GEN=2/4/5 pins one (A/B).
 #ifndef IFKV_ATTN_GEN
 #define IFKV_ATTN_GEN 0
 #endif
@@ -131,8 +135,11 @@ static int recompute_attn_tc_any(const void* q, const void* k_layer, const void*
     // v4 also when the GQA group does not tile 128 rows evenly (Qwen2.5: G = 7,
     // 18 tokens x 7 heads = 126 rows): 1.25 vs 1.34 ms at k = 4916, 32K keys
     const int G = Hkv > 0 ? H / Hkv : 1;
-    gen = ((int64_t)Hkv * pairs >= 2 * sms && G > 0 && 128 % G == 0) ? 2 : 4;
+    gen = ((int64_t)Hkv * pairs >= 2 * sms && G > 0 && 128 % G == 0) ? 5 : 4;
   }
+  if (gen == 5)
+    return ifkv_recompute_attn_tc_v5(q, k_layer, v_layer, horizon, S, H, Hkv, Dh, n_rows, scale, out, ml_out,
+                                     stream);
   if (gen == 4)
     return ifkv_recompute_attn_tc_v4(q, k_layer, v_layer, horizon, S, H, Hkv, Dh, n_rows, scale, out, ml_out,
                                      stream);
