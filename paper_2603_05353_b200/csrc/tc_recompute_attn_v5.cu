@@ -26,6 +26,9 @@ constexpr int kTile = 2 * kPanel;  // 32 KB
 constexpr int kSlots = 3;
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleLog2 = 8.0f;
+#ifndef IFKV_ATTN5_ONEPASS
+#define IFKV_ATTN5_ONEPASS 0
+#endif
 
 struct Smem {
   uint8_t q[2][kTile];
@@ -73,6 +76,74 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
     tc::tc_fence_after();
     const int j0 = (b0 + j) * kKeys;
     const bool masked = __any_sync(0xffffffffu, j0 + kKeys - 1 > hz);
+#if IFKV_ATTN5_ONEPASS
+    // one TMEM read of the whole S row; S_x(j+1) may start right after it
+    float v[128];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tc::tmem_ld32(t_s + 32 * q, v + 32 * q);
+    tc::tmem_ld_wait();
+    tc::tc_fence_before();
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(&sm.s_free[x]);
+    if (masked) {
+#pragma unroll
+      for (int c = 0; c < 128; ++c)
+        if (j0 + c > hz) v[c] = -INFINITY;
+    }
+    float mx = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < 128; c += 2) mx = tc::max3(mx, v[c], v[c + 1]);
+    float alpha = 1.f;
+    bool need = false;
+    if (mx > -INFINITY && (m_used == -INFINITY || (mx - m_used) * scale_log2 > kRescaleLog2)) {
+      need = true;
+      alpha = m_used == -INFINITY ? 0.f : tc::ex2((m_used - mx) * scale_log2);
+      m_used = mx;
+    }
+    const float mb = m_used == -INFINITY ? 0.f : m_used * scale_log2;
+    if (j > 0) {
+      tc::mbar_wait(&sm.pv_done[x][(j - 1) & 1], ((j - 1) >> 1) & 1);
+      tc::tc_fence_after();
+    }
+    if (j > 0 && __any_sync(0xffffffffu, need)) {
+      const float a = need ? alpha : 1.f;
+#pragma unroll 1
+      for (int c = 0; c < kDh / 16; ++c) {
+        float o[16];
+        tc::tmem_ld16(t_o + c * 16, o);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 16; ++u) o[u] *= a;
+        tc::tmem_st16(t_o + c * 16, reinterpret_cast<const uint32_t*>(o));
+      }
+      tc::tmem_st_wait();
+    }
+    float sum = 0.f;
+    const float2 sc2 = make_float2(scale_log2, scale_log2), mb2 = make_float2(-mb, -mb);
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      float2 sum2 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int c8 = 0; c8 < 8; ++c8) {
+        uint4 pk;
+        uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = hf * 64 + c8 * 8 + 2 * u;
+          const float2 xx = tc::ffma2(make_float2(v[c], v[c + 1]), sc2, mb2);
+          const float2 e = make_float2(tc::ex2(xx.x), tc::ex2(xx.y));
+          sum2 = tc::fadd2(sum2, e);
+          pw[u] = tc::pack_bf16(e.x, e.y);
+        }
+        st_p_chunk(P, row, hf, c8, pk);
+      }
+      sum += sum2.x + sum2.y;
+      tc::fence_async_smem();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&sm.p_full[x][hf]);
+    }
+#else
     float v[64];
     float mx = -INFINITY;
 #pragma unroll
@@ -160,6 +231,7 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&sm.p_full[x][hf]);
     }
+#endif
     l = l * alpha + sum;
   }
   if (nblk > 0) {
