@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--model", default="llama3_8b")
     ap.add_argument("--reorder", action="store_true")
     ap.add_argument("--out", default="gpurun_out/timeline.json")
+    ap.add_argument("--steps", type=int, default=1, help="back-to-back steps inside the capture")
     args = ap.parse_args()
     cfg = bench.model_config(args)
     weights = P.DeviceWeights.random(cfg, seed=7, precision="bf16")
@@ -45,7 +46,8 @@ def main():
     from torch.profiler import ProfilerActivity, profile
 
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
-        step()
+        for _ in range(args.steps):
+            step()
         torch.cuda.synchronize()
     evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
     ks = []
