@@ -235,3 +235,22 @@ def test_recompute_attention_large_grid_v2_path(T, cuda, partial):
     assert np.max(np.abs(got[pick] - want)) <= 1e-2 * np.max(np.abs(want))
     if partial:
         assert np.all(got[:70] == 0)
+
+
+@pytest.mark.parametrize("H,hkv,k", [(28, 4, 300), (28, 4, 2600), (24, 8, 2600)])
+def test_recompute_attention_gqa_groups_not_dividing_128(T, cuda, H, hkv, k):
+    """G = 7 (Qwen2.5-VL: 18 tokens x 7 heads = 126 rows per tile, v4 path) and
+    G = 3 (42 tokens x 3 heads) against the oracle on sampled rows."""
+    from paper_2603_05353_b200 import engine as E
+
+    rng = np.random.default_rng(H + k)
+    dh, n = 128, 5000
+    hz = np.sort(rng.choice(n, k, replace=False))
+    q = T.as_tensor(rng.standard_normal((k, H, dh)), dtype=T.float32).to(cuda, T.bfloat16)
+    kk = T.as_tensor(rng.standard_normal((n, hkv, dh)), dtype=T.float32).to(cuda, T.bfloat16)
+    vv = T.as_tensor(rng.standard_normal((n, hkv, dh)), dtype=T.float32).to(cuda, T.bfloat16)
+    got = E.recompute_attn(q, kk, vv, T.as_tensor(hz, device=cuda), H, hkv, dh).double().cpu().numpy()
+    pick = np.sort(rng.choice(k, 40, replace=False))
+    want, _ = O.prefix_attention(q.double().cpu().numpy()[pick], kk.double().cpu().numpy(),
+                                 vv.double().cpu().numpy(), hz[pick])
+    assert np.max(np.abs(got[pick] - want)) <= 1e-2 * np.max(np.abs(want))
