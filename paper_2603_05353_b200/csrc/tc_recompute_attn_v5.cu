@@ -26,6 +26,12 @@ constexpr int kTile = 2 * kPanel;  // 32 KB
 constexpr int kSlots = 3;
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleLog2 = 8.0f;
+#ifndef IFKV_ATTN5_DYN
+#define IFKV_ATTN5_DYN 0
+#endif
+#ifndef IFKV_ATTN5_XORDER
+#define IFKV_ATTN5_XORDER 0
+#endif
 #ifndef IFKV_ATTN5_ONEPASS
 #define IFKV_ATTN5_ONEPASS 0
 #endif
@@ -39,6 +45,16 @@ struct Smem {
   uint32_t tmem_base;
   int n_blocks[2];
 };
+
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(tc::smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 
 // Load order of the K/V ring: K(0), then for j >= 0: K(j+1), V(j) (and finally
 // V(n-1)).  Item i of that order occupies slot i % kSlots; the MMA warp frees
@@ -387,6 +403,72 @@ __global__ void __launch_bounds__(384, 1)
       for (int x = 0; x < 2; ++x)
         if ((x == 0 ? nA : nB) > 0) issue_s(x, 0);
       tc::mma_commit_ws(&sm.empty[item_of_k(0) % kSlots]);
+#if IFKV_ATTN5_DYN  // A/B: event-driven issue -- whichever S / PV half of either tile is ready
+      {
+        const int n_of[2] = {nA, nB};
+        int s_next[2] = {1, 1}, pv_next[2] = {0, 0}, half[2] = {0, 0};
+        auto k_ready = [&](int j) {
+          const int i = item_of_k(j);
+          return mbar_test(&sm.full[i % kSlots], (i / kSlots) & 1);
+        };
+        auto v_ready = [&](int j) {
+          const int i = item_of_v(j);
+          return mbar_test(&sm.full[i % kSlots], (i / kSlots) & 1);
+        };
+        while (pv_next[0] < n_of[0] || pv_next[1] < n_of[1]) {
+#pragma unroll
+          for (int x = 0; x < 2; ++x) {
+            const int y = x ^ 1;
+            if (s_next[x] < n_of[x]) {
+              const int j = s_next[x];
+              if (mbar_test(&sm.s_free[x], (j - 1) & 1) && k_ready(j)) {
+                tc::tc_fence_after();
+                issue_s(x, j);
+                ++s_next[x];
+                if (s_next[y] > j || n_of[y] <= j) tc::mma_commit_ws(&sm.empty[item_of_k(j) % kSlots]);
+              }
+            }
+            if (pv_next[x] < n_of[x]) {
+              const int j = pv_next[x];
+              if (mbar_test(&sm.p_full[x][half[x]], j & 1) && v_ready(j)) {
+                tc::tc_fence_after();
+                issue_pv_half(x, j, half[x]);
+                if (++half[x] == 2) {
+                  half[x] = 0;
+                  tc::mma_commit_ws(&sm.pv_done[x][j & 1]);
+                  if (j == n_of[x] - 1) tc::mma_commit_ws(&sm.o_final[x]);
+                  ++pv_next[x];
+                  if (pv_next[y] > j || n_of[y] <= j) tc::mma_commit_ws(&sm.empty[item_of_v(j) % kSlots]);
+                }
+              }
+            }
+          }
+        }
+      }
+#else
+#if IFKV_ATTN5_XORDER  // A/B: per tile, S_x(j+1) then PV_x(j), tile A then tile B
+      for (int j = 0; j < nblk; ++j) {
+        if (j + 1 < nblk) wait_item(item_of_k(j + 1));
+        wait_item(item_of_v(j));
+        for (int x = 0; x < 2; ++x) {
+          const int nx = x == 0 ? nA : nB;
+          if (j + 1 < nx) {
+            tc::mbar_wait(&sm.s_free[x], j & 1);
+            tc::tc_fence_after();
+            issue_s(x, j + 1);
+          }
+          if (j < nx) {
+            for (int hf = 0; hf < 2; ++hf) {
+              tc::mbar_wait(&sm.p_full[x][hf], j & 1);
+              tc::tc_fence_after();
+              issue_pv_half(x, j, hf);
+            }
+            tc::mma_commit_ws(&sm.pv_done[x][j & 1]);
+            if (j == nx - 1) tc::mma_commit_ws(&sm.o_final[x]);
+          }
+        }
+        if (j + 1 < nblk) tc::mma_commit_ws(&sm.empty[item_of_k(j + 1) % kSlots]);
+#else
       for (int j = 0; j < nblk; ++j) {
         // S_x(j+1) as soon as the softmax has read S_x(j)
         if (j + 1 < nblk) {
@@ -412,8 +494,10 @@ __global__ void __launch_bounds__(384, 1)
           tc::mma_commit_ws(&sm.pv_done[x][j & 1]);
           if (j == nx - 1) tc::mma_commit_ws(&sm.o_final[x]);
         }
+#endif
         tc::mma_commit_ws(&sm.empty[item_of_v(j) % kSlots]);
       }
+#endif  // IFKV_ATTN5_DYN
     }
   } else {
     const int x = (warp - 4) >> 2;
