@@ -116,7 +116,8 @@ extern "C" int ifkv_recompute_attn_tc_v5(const void* q, const void* k_layer, con
                                          float scale, void* out, float* ml_out, void* stream);
 // tcgen05 kernel generation: v5 (two ping-ponging tiles per CTA, P staged in
 // smem so S(j+1) follows the read of S(j); 3-5 % faster than v2, identical
-// results) while the grid fills two waves of the GPU and G divides 128, else v4 (one tile per CTA, double-buffered
+// results; GQA groups padded to a power of two) while the grid fills two waves
+// of the GPU, else v4 (one tile per CTA, double-buffered
 // S, column-split softmax: twice the CTAs; measured 0.474 vs 0.574 ms at
 // k = 1639, 0.650 vs 0.624 ms at k = 2458).  IFKV_ATTN_GEN=2/4/5 pins one (A/B).
 #ifndef IFKV_ATTN_GEN
@@ -130,12 +131,11 @@ static int recompute_attn_tc_any(const void* q, const void* k_layer, const void*
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int per_pair = Hkv > 0 && H % Hkv == 0 ? 2 * (128 / (H / Hkv)) : 1;
+    int Gp = 1;  // v5 pads the GQA group to a power of two (zero query rows)
+    while (Hkv > 0 && Gp < H / Hkv) Gp *= 2;
+    const int per_pair = 2 * (128 / Gp);
     const int64_t pairs = ((int64_t)S + per_pair - 1) / per_pair;
-    // v4 also when the GQA group does not tile 128 rows evenly (Qwen2.5: G = 7,
-    // 18 tokens x 7 heads = 126 rows): 1.25 vs 1.34 ms at k = 4916, 32K keys
-    const int G = Hkv > 0 ? H / Hkv : 1;
-    gen = ((int64_t)Hkv * pairs >= 2 * sms && G > 0 && 128 % G == 0) ? 5 : 4;
+    gen = (int64_t)Hkv * pairs >= 2 * sms ? 5 : 4;
   }
   if (gen == 5)
     return ifkv_recompute_attn_tc_v5(q, k_layer, v_layer, horizon, S, H, Hkv, Dh, n_rows, scale, out, ml_out,

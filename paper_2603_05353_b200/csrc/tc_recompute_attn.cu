@@ -107,7 +107,7 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
   const int row = w * 32 + lane;
   const int tok = t0 + row / G;
   const bool valid = row < (kRows / G) * G && tok < S;  // G not dividing 128 leaves pad rows
-  const int hz = valid ? (int)horizon[tok] : 0;
+  const int hz = valid ? (int)horizon[tok] : INT_MAX;  // pad rows: never force the masked path
   const uint32_t lane_off = (uint32_t)(w * 32) << 16;
   const uint32_t t_s = tmem + 256 * x + lane_off;
   const uint32_t t_o = t_s + 128;

@@ -79,7 +79,7 @@ __device__ __forceinline__ void softmax_half(Smem& sm, uint32_t tmem, int hf, in
   const int row = q * 32 + lane;
   const int tok = t0 + row / G;
   const bool valid = row < (kRows / G) * G && tok < S;
-  const int hz = valid ? (int)horizon[tok] : 0;
+  const int hz = valid ? (int)horizon[tok] : INT_MAX;  // pad rows: never force the masked path
   const uint32_t lane_off = (uint32_t)(q * 32) << 16;
   const uint32_t t_o = tmem + kColO + lane_off + 64 * hf;
   const int bar_id = 1 + q;

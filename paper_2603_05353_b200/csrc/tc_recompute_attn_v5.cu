@@ -74,14 +74,17 @@ __device__ __forceinline__ void st_p_chunk(uint8_t* p, int r, int panel, int c, 
 }
 
 __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int nblk, int b0, int t0, int S, int H,
-                                             int G, int g, const int64_t* __restrict__ horizon, float scale_log2,
+                                             int G, int Gp, int g, const int64_t* __restrict__ horizon,
+                                             float scale_log2,
                                              __nv_bfloat16* __restrict__ out, float* __restrict__ ml_out) {
   const int w = (threadIdx.x >> 5) & 3;
   const int lane = threadIdx.x & 31;
   const int row = w * 32 + lane;
-  const int tok = t0 + row / G;
-  const bool valid = row < (kRows / G) * G && tok < S;
-  const int hz = valid ? (int)horizon[tok] : 0;
+  // tile row = token (row / Gp) x head of the group (row % Gp); Gp is G rounded
+  // up to a power of two -- the padded heads are zero query rows (TMA OOB fill)
+  const int tok = t0 + row / Gp;
+  const bool valid = row % Gp < G && tok < S;
+  const int hz = valid ? (int)horizon[tok] : INT_MAX;  // pad rows: never force the masked path
   const uint32_t lane_off = (uint32_t)(w * 32) << 16;
   const uint32_t t_s = tmem + 256 * x + lane_off;
   const uint32_t t_o = t_s + 128;
@@ -255,7 +258,7 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
     tc::tc_fence_after();
   }
   const float inv = l > 0.f ? 1.f / l : 0.f;
-  const int64_t orow = (int64_t)tok * H + g * G + row % G;
+  const int64_t orow = (int64_t)tok * H + g * G + row % Gp;
   __nv_bfloat16* dst = out + orow * kDh;
   if (ml_out && valid) {
     ml_out[2 * orow] = m_used == -INFINITY ? -INFINITY : m_used * scale_log2 * 0.6931471805599453f;
@@ -288,13 +291,13 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
 __global__ void __launch_bounds__(384, 1)
     recompute_attn_v5_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                              const __grid_constant__ CUtensorMap tm_v, const int64_t* __restrict__ horizon, int S,
-                             int H, int Hkv, float scale_log2, __nv_bfloat16* __restrict__ out,
+                             int H, int Hkv, int Gp, float scale_log2, __nv_bfloat16* __restrict__ out,
                              float* __restrict__ ml_out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = H / Hkv;
-  const int tok = kRows / G;
+  const int tok = kRows / Gp;
   const int g = blockIdx.x;
   const int pair = gridDim.y - 1 - blockIdx.y;
   const int tA = pair * 2 * tok, tB = tA + tok;
@@ -341,12 +344,12 @@ __global__ void __launch_bounds__(384, 1)
       tc::tma_prefetch(&tm_q);
       tc::tma_prefetch(&tm_k);
       tc::tma_prefetch(&tm_v);
-      tc::mbar_arrive_expect_tx(&sm.q_full, (nB > 0 ? 2 : 1) * 2 * 128 * (tok * G));
-      tc::tma_load_3d(sm.q[0], &tm_q, &sm.q_full, 0, g * G, tA);
-      tc::tma_load_3d(sm.q[0] + kPanel, &tm_q, &sm.q_full, 64, g * G, tA);
+      tc::mbar_arrive_expect_tx(&sm.q_full, (nB > 0 ? 2 : 1) * kTile);  // box = tok x Gp = 128 rows
+      tc::tma_load_4d(sm.q[0], &tm_q, &sm.q_full, 0, 0, g, tA);
+      tc::tma_load_4d(sm.q[0] + kPanel, &tm_q, &sm.q_full, 64, 0, g, tA);
       if (nB > 0) {
-        tc::tma_load_3d(sm.q[1], &tm_q, &sm.q_full, 0, g * G, tB);
-        tc::tma_load_3d(sm.q[1] + kPanel, &tm_q, &sm.q_full, 64, g * G, tB);
+        tc::tma_load_4d(sm.q[1], &tm_q, &sm.q_full, 0, 0, g, tB);
+        tc::tma_load_4d(sm.q[1] + kPanel, &tm_q, &sm.q_full, 64, 0, g, tB);
       }
       // items in order K0, K1, V0, K2, V1, ..., K(n-1), V(n-2), V(n-1)
       const int n_items = 2 * nblk;
@@ -503,7 +506,7 @@ __global__ void __launch_bounds__(384, 1)
     const int x = (warp - 4) >> 2;
     const int nx = x == 0 ? nA : nB;
     const int tx = x == 0 ? tA : tB;
-    if (tx < S) softmax_tile(sm, tmem, x, nx, b0, tx, S, H, G, g, horizon, scale_log2, out, ml_out);
+    if (tx < S) softmax_tile(sm, tmem, x, nx, b0, tx, S, H, G, Gp, g, horizon, scale_log2, out, ml_out);
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -521,12 +524,16 @@ extern "C" int ifkv_recompute_attn_tc_v5(const void* q, const void* k_layer, con
   IFKV_CHECK_ARG(Dh == kDh && Hkv > 0 && H % Hkv == 0 && H / Hkv <= 16, "recompute_attn_v5: unsupported shape");
   if (S <= 0) return IFKV_OK;
   const int G = H / Hkv;
+  int Gp = 1;
+  while (Gp < G) Gp *= 2;  // heads per tile row group, padded to a power of two
   CUtensorMap tq, tk, tv;
   {
-    uint64_t dims[3] = {(uint64_t)Dh, (uint64_t)H, (uint64_t)S};
-    uint64_t strides[2] = {(uint64_t)Dh * 2, (uint64_t)H * Dh * 2};
-    uint32_t box[3] = {64, (uint32_t)G, (uint32_t)(kRows / G)};
-    int rc = make_tmap_bf16(&tq, q, 3, dims, strides, box);
+    // q [S][Hkv][G][Dh] viewed 4-D; the box takes Gp >= G heads: rows of
+    // heads G..Gp-1 fall outside the tensor and are zero-filled by TMA
+    uint64_t dims[4] = {(uint64_t)Dh, (uint64_t)G, (uint64_t)Hkv, (uint64_t)S};
+    uint64_t strides[3] = {(uint64_t)Dh * 2, (uint64_t)G * Dh * 2, (uint64_t)H * Dh * 2};
+    uint32_t box[4] = {64, (uint32_t)Gp, 1, (uint32_t)(kRows / Gp)};
+    int rc = make_tmap_bf16(&tq, q, 4, dims, strides, box);
     if (rc) return rc;
   }
   {
@@ -542,11 +549,11 @@ extern "C" int ifkv_recompute_attn_tc_v5(const void* q, const void* k_layer, con
   IFKV_CUDA_CALL(cudaFuncSetAttribute(recompute_attn_v5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem),
                  "recompute_attn_v5: smem attribute");
-  const int per_pair = 2 * (kRows / G);
+  const int per_pair = 2 * (kRows / Gp);
   const int pairs = (S + per_pair - 1) / per_pair;
   const float scale_log2 = scale * 1.4426950408889634f;
   recompute_attn_v5_kernel<<<dim3(Hkv, pairs, 1), 384, smem, as_stream(stream)>>>(
-      tq, tk, tv, horizon, S, H, Hkv, scale_log2, (__nv_bfloat16*)out, ml_out);
+      tq, tk, tv, horizon, S, H, Hkv, Gp, scale_log2, (__nv_bfloat16*)out, ml_out);
   IFKV_LAUNCH_CHECK("recompute_attn_v5");
   return IFKV_OK;
 }
