@@ -108,7 +108,24 @@ def ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
 
-def stream_handle() -> int:
-    import torch
+_stream_fn = None
 
-    return torch.cuda.current_stream().cuda_stream
+
+def stream_handle() -> int:
+    """The current CUDA stream of the current device (raw cudaStream_t).
+    Uses torch's direct C accessors when present: torch.cuda.current_stream()
+    costs several microseconds of Python per call (device-index resolution,
+    availability checks) and the scoring pass makes ~12 entry-point calls
+    per layer, so on a synchronous query it was a visible share of the host
+    time that paces the GPU."""
+    global _stream_fn
+    if _stream_fn is None:
+        import torch
+
+        raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+        dev = getattr(torch._C, "_cuda_getDevice", None)
+        if raw is not None and dev is not None:
+            _stream_fn = lambda: raw(dev())  # noqa: E731
+        else:  # pragma: no cover - older torch
+            _stream_fn = lambda: torch.cuda.current_stream().cuda_stream  # noqa: E731
+    return _stream_fn()

@@ -254,3 +254,13 @@ def test_recompute_attention_gqa_groups_not_dividing_128(T, cuda, H, hkv, k):
     want, _ = O.prefix_attention(q.double().cpu().numpy()[pick], kk.double().cpu().numpy(),
                                  vv.double().cpu().numpy(), hz[pick])
     assert np.max(np.abs(got[pick] - want)) <= 1e-2 * np.max(np.abs(want))
+
+
+def test_stream_handle_follows_torch_current_stream(T, cuda):
+    from paper_2603_05353_b200 import _native as N
+
+    assert N.stream_handle() == T.cuda.current_stream().cuda_stream
+    s = T.cuda.Stream()
+    with T.cuda.stream(s):
+        assert N.stream_handle() == s.cuda_stream
+    assert N.stream_handle() == T.cuda.current_stream().cuda_stream

@@ -49,3 +49,59 @@ def test_sharded_select_and_recompute_match_oracle(cuda, world):
     assert rel_err(full_scores, scores) <= 1e-4
     assert rel_err(gk, wk[:, :2048]) <= 1e-2
     assert rel_err(gv, wv[:, :2048]) <= 1e-2
+
+
+def test_torchcomm_nccl_single_rank_path(cuda):
+    """The TorchComm code path over a real NCCL communicator (world 1: every
+    collective still runs through NCCL -- all_gather, variable-size gathers,
+    list all_to_all with uneven and empty parts) end to end at C1, against
+    the oracle.  Multi-GPU NCCL itself needs more than the one GPU here."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2603_05353_b200 as P
+    from paper_2603_05353_b200 import sharding as SH
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        comm = SH.TorchComm()
+        a = torch.arange(12, dtype=torch.float32, device="cuda").view(6, 2)
+        got = comm.all_to_all([a])
+        assert torch.equal(got[0], a)
+        e = comm.all_to_all([a[:0]])
+        assert e[0].shape == (0, 2)
+        gv = comm.all_gather_var(a[:5])
+        assert torch.equal(gv[0], a[:5])
+
+        cfg = P.c1_config()
+        dw = P.DeviceWeights.from_host(P.init_weights(cfg, 7), "bf16")
+        ow = dw.to_host()
+        task = P.SyntheticTask(kind="uniform_noise", total_length=2048, fixed_size=256, prompt_length=32,
+                               vocab_size=1024)
+        g = P.generate_task(task, 2)
+        kvs = [P.prefill_chunk(dw, c) for c in g.chunks]
+        oc = O.assemble([oracle_chunk(c) for c in kvs])
+        scores, sel = O.run_selection(ow, oc, g.prompt_token_ids, ratio=0.15)
+        want = O.recompute_selected(ow, oc, *O.make_plan(oc.context_length, sel))
+        wk, wv = O.decode_view(want, cfg.rope_base)
+        shard = SH.make_shard([c.length for c in kvs], 0, 1)
+        local = P.assemble([kvs[i] for i in shard.chunk_ids])
+        res = SH.sharded_select(dw, shard, local, g.prompt_token_ids, P.SelectionConfig(ratio=0.15), comm)
+        SH.sharded_recompute(dw, shard, local, res.selected, comm)
+        np.testing.assert_array_equal(res.selected.cpu().numpy(), sel)
+        full = np.zeros(2048)
+        full[shard.global_rows] = res.scores.double().cpu().numpy()
+        assert rel_err(full, scores) <= 1e-4
+        lk = np.zeros_like(wk[:, :2048])
+        lk[:, shard.global_rows] = to_np(local.keys)
+        assert rel_err(lk, wk[:, :2048]) <= 1e-2
+    finally:
+        dist.destroy_process_group()
