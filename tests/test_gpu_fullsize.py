@@ -1,5 +1,6 @@
 """Parity at BASELINE.json's full size (C2: Llama-3-8B shape, 32 layers, 32K
-context in 16 x 2048 chunks, 32-token prompt, r = 0.15).  The oracle cannot
+context in 16 x 2048 chunks, 32-token prompt, r = 0.15; and C4, the
+Qwen2.5-VL-7B LM shape).  The oracle cannot
 run the path at this size in test time, so these tests check the
 size-independent properties the reference's own tests pin
 (SURVEY §8c), on the GPU path through the public API:
@@ -25,14 +26,23 @@ pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 N_CTX, CHUNK, M, RATIO = 32768, 2048, 32, 0.15
 
 
-@pytest.fixture(scope="module")
-def c2(cuda):
+@pytest.fixture(scope="module", params=["llama3_8b", "qwen25vl_7b"])
+def c2(cuda, request):
+    """C2 (Llama-3-8B shape) and C4 (Qwen2.5-VL-7B LM shape: GQA group 7,
+    24 x 1280 image-token chunks + 4 x 512 text chunks)."""
     import paper_2603_05353_b200 as P
 
-    cfg = P.llama3_8b_config()
+    if request.param == "llama3_8b":
+        cfg = P.llama3_8b_config()
+        task = P.SyntheticTask(kind="uniform_noise", total_length=N_CTX, fixed_size=CHUNK, prompt_length=M,
+                               vocab_size=cfg.vocab_size)
+    else:
+        cfg = P.qwen25vl_7b_config()
+        lens = [1280] * 24 + [512] * 4
+        task = P.SyntheticTask(kind="uniform_noise", total_length=N_CTX, fixed_size=None,
+                               boundaries=tuple(np.cumsum(lens)[:-1].tolist()), prompt_length=M,
+                               vocab_size=cfg.vocab_size)
     w = P.DeviceWeights.random(cfg, seed=7, precision="bf16")
-    task = P.SyntheticTask(kind="uniform_noise", total_length=N_CTX, fixed_size=CHUNK, prompt_length=M,
-                           vocab_size=cfg.vocab_size)
     gen = P.generate_task(task, seed=0)
     kvs = [P.prefill_chunk(w, c) for c in gen.chunks]
     return P, cfg, w, gen, kvs
