@@ -97,6 +97,14 @@ int ifkv_split3(const float* x, int64_t n, void* out, void* stream);
  * CacheBlend baseline's per-token hidden-state deviation
  * (replaces np.linalg.norm in selection.py:219-222). */
 int ifkv_row_dist_accum(const float* a, const float* b, int rows, int d, double* acc, void* stream);
+/* Prompt-row GEMM of the scoring pass (x @ W of model.py:435-455 for the M
+ * prompt rows, selection.py:127-169): out[s][r][n] = sum_{p<P} sum_{k in
+ * split s} x[p][r][k] w[k][n]; x bf16 [P][R][K] (the split3 terms), w bf16
+ * [K][N] row-major, out fp32 [splits][R][N] (per-split partials, summed by the
+ * consumer's n_parts).  R % 32 == 0, P*R <= 256, K % 64 == 0, N % 128 == 0,
+ * 1 <= splits <= K/64.  HBM-bound weight stream on tcgen05 (replaces the
+ * cuBLAS calls of the scoring layers). */
+int ifkv_prompt_mm(const void* x, int P, int R, int K, const void* w, int N, int splits, float* out, void* stream);
 
 /* ---- fresh q/k/v (model.py:433-437, recompute.py:99-112) ----------------
  * qkv = [rows][(H + 2 Hkv) Dh] (GEMM output, qkv_dtype, n_parts part blocks

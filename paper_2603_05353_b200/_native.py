@@ -33,6 +33,7 @@ SIGNATURES = {
     "ifkv_embed_rows": [P, I32, P, I32, I32, P, P],
     "ifkv_split3": [P, I64, P, P],
     "ifkv_row_dist_accum": [P, P, I32, I32, P, P],
+    "ifkv_prompt_mm": [P, I32, I32, I32, P, I32, I32, P, P],
     "ifkv_qkv_rope_scatter": [P, I32, I32, I32, I32, I32, I32, P, I32, P, P, P, P, P],
     "ifkv_prompt_attn_partial": [I32, P, P, P, P, P, P, I32, I32, I32, I32, I32, I32, F32, P, P, P],
     "ifkv_prompt_attn_merge": [P, P, P, I32, I32, I32, I32, I32, P, P, P, P],

@@ -244,10 +244,51 @@ def recompute_attn(q, k_layer, v_layer, horizon, H, Hkv, Dh, out=None, impl: str
 # ---------------------------------------------------------------------------
 
 
+# Scoring-pass GEMMs of the prompt rows on our tcgen05 weight-stream kernel
+# (ifkv_prompt_mm) instead of cuBLAS; IFKV_PROMPT_MM=0 restores cuBLAS (A/B).
+PROMPT_MM = os.environ.get("IFKV_PROMPT_MM", "1") != "0"
+_SMS: List[int] = []
+
+
+def _sm_count() -> int:
+    if not _SMS:
+        torch = _torch()
+        _SMS.append(torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count)
+    return _SMS[0]
+
+
+def prompt_mm_splits(N: int, K: int, R: int, sms: int, P: int = 3) -> int:
+    """K splits of ifkv_prompt_mm: as many (n-tile, split) CTAs as fit in ONE
+    wave (a second, partial wave of a weight stream costs more than the
+    split partials; measured in tools/prompt_mm_bench.py), >= 2 k-steps each."""
+    n_tiles, k_steps = N // 128, K // 64
+    per_sm = 2 if 3 * (16384 + P * R * 128) + 2048 <= 113 * 1024 else 1  # 3-stage ring per CTA
+    return max(1, min((per_sm * sms) // n_tiles, k_steps // 2))
+
+
+def prompt_mm_ok(x, w) -> bool:
+    torch = _torch()
+    if not (PROMPT_MM and x.dim() == 3 and x.dtype == torch.bfloat16 and w.dtype == torch.bfloat16):
+        return False
+    p, rows, k = x.shape
+    return (rows % 32 == 0 and p * rows <= 256 and k % 64 == 0 and w.shape[0] == k and w.shape[1] % 128 == 0
+            and x.is_contiguous() and w.is_contiguous())
+
+
 def mm_parts(x, w):
     """x: [P, rows, K] (bf16 split terms) or [rows, K] fp32; returns fp32
-    [P, rows, N] (sum the P blocks downstream) -- exact products, fp32 sums."""
+    [n, rows, N] part blocks whose sum is x @ w (consumers sum the n blocks):
+    exact products, fp32 sums.  Prompt-row shapes run on ifkv_prompt_mm
+    (n = its K splits, the P terms summed in its epilogue), others on cuBLAS
+    (n = P)."""
     torch = _torch()
+    if prompt_mm_ok(x, w):
+        p, rows, k = x.shape
+        n = w.shape[1]
+        s = prompt_mm_splits(n, k, rows, _sm_count(), p)
+        out = torch.empty((s, rows, n), dtype=torch.float32, device=x.device)
+        N.call("ifkv_prompt_mm", N.ptr(x), p, rows, k, N.ptr(w), n, s, N.ptr(out), _s())
+        return out
     if x.dim() == 3:
         p, rows, k = x.shape
         y = torch.mm(x.reshape(p * rows, k), w, out_dtype=torch.float32)

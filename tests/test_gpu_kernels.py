@@ -264,3 +264,34 @@ def test_stream_handle_follows_torch_current_stream(T, cuda):
     with T.cuda.stream(s):
         assert N.stream_handle() == s.cuda_stream
     assert N.stream_handle() == T.cuda.current_stream().cuda_stream
+
+
+@pytest.mark.parametrize("P,R,K,N", [(3, 32, 4096, 6144), (3, 32, 14336, 4096), (1, 32, 512, 1536),
+                                     (3, 64, 512, 3584), (2, 96, 1024, 256)])
+def test_prompt_mm_weight_stream_gemm(T, cuda, P, R, K, N):
+    """ifkv_prompt_mm (tcgen05, MN-major weight operand, K splits) against
+    an fp64 product of the same bf16 operands: fp32 accumulation only."""
+    from paper_2603_05353_b200 import _native as NV
+    from paper_2603_05353_b200 import engine as E
+
+    g = T.Generator(device="cuda").manual_seed(P * 1000 + R)
+    x = T.randn(P, R, K, device="cuda", generator=g).to(T.bfloat16)
+    w = (T.randn(K, N, device="cuda", generator=g) / math.sqrt(K)).to(T.bfloat16)
+    want = sum(x[p].double() @ w.double() for p in range(P))
+
+    def rel(got):
+        return float((got - want).abs().max() / want.abs().max())
+
+    # tolerance: fp32 accumulation over K, calibrated on cuBLAS's own error
+    # for the same bf16 operands (~1e-5 at K = 14336)
+    cub = rel(sum(T.mm(x[p], w, out_dtype=T.float32).double() for p in range(P)))
+    tol = max(1e-5, 2 * cub)
+    for s in sorted({1, E.prompt_mm_splits(N, K, R, 148, P), min(K // 64, 7)}):
+        out = T.full((s, R, N), float("nan"), dtype=T.float32, device="cuda")
+        NV.call("ifkv_prompt_mm", NV.ptr(x), P, R, K, NV.ptr(w), N, s, NV.ptr(out), NV.stream_handle())
+        assert rel(out.double().sum(0)) < tol, (s, cub)
+    assert rel(E.mm_parts(x, w).double().sum(0)) < tol
+    from paper_2603_05353_b200.errors import ConfigurationError
+
+    with pytest.raises(ConfigurationError):
+        NV.call("ifkv_prompt_mm", NV.ptr(x), P, 16, K, NV.ptr(w), N, 1, NV.ptr(out), NV.stream_handle())
