@@ -116,10 +116,13 @@ extern "C" int ifkv_recompute_attn_tc_v5(const void* q, const void* k_layer, con
                                          float scale, void* out, float* ml_out, void* stream);
 // tcgen05 kernel generation: v5 (two ping-ponging tiles per CTA, P staged in
 // smem so S(j+1) follows the read of S(j); 3-5 % faster than v2, identical
-// results; GQA groups padded to a power of two) while the grid fills two waves
-// of the GPU, else v4 (one tile per CTA, double-buffered
-// S, column-split softmax: twice the CTAs; measured 0.474 vs 0.574 ms at
-// k = 1639, 0.650 vs 0.624 ms at k = 2458).  IFKV_ATTN_GEN=2/4/5 pins one (A/B).
+// results; GQA groups padded to a power of two; key splits below two waves),
+// except for a padded group (G = 7: 1/8 of v5's rows are zeros) on a grid
+// under two waves, where v4 (one tile per CTA, triple-buffered S, column-split
+// softmax, key splits) is 2.5 % faster.  v5 vs v4 at G = 4 (ms per layer,
+// C2 shape): k = 1639 0.445-0.48 vs 0.47-0.52, k = 2458 0.57-0.64 vs
+// 0.64-0.74, k = 3277 0.79-0.94 vs 0.84-0.98, k = 4916 1.07-1.20 vs 1.23-1.42
+// (profiles/r1_attn_ab.md).  IFKV_ATTN_GEN=2/4/5 pins one (A/B).
 #ifndef IFKV_ATTN_GEN
 #define IFKV_ATTN_GEN 0
 #endif
@@ -135,7 +138,8 @@ static int recompute_attn_tc_any(const void* q, const void* k_layer, const void*
     while (Hkv > 0 && Gp < H / Hkv) Gp *= 2;
     const int per_pair = 2 * (128 / Gp);
     const int64_t pairs = ((int64_t)S + per_pair - 1) / per_pair;
-    gen = (int64_t)Hkv * pairs >= 2 * sms ? 5 : 4;
+    const bool padded = Hkv > 0 && Gp != H / Hkv;  // v5 computes zero rows for G < Gp
+    gen = (!padded || (int64_t)Hkv * pairs >= 2 * sms) ? 5 : 4;
   }
   if (gen == 5)
     return ifkv_recompute_attn_tc_v5(q, k_layer, v_layer, horizon, S, H, Hkv, Dh, n_rows, scale, out, ml_out,

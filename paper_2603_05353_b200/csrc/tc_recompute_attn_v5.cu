@@ -35,6 +35,9 @@ constexpr float kRescaleLog2 = 8.0f;
 #ifndef IFKV_ATTN5_ONEPASS
 #define IFKV_ATTN5_ONEPASS 0
 #endif
+#ifndef IFKV_ATTN5_SPLITS
+#define IFKV_ATTN5_SPLITS 1
+#endif
 
 struct Smem {
   uint8_t q[2][kTile];
@@ -513,6 +516,40 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 2) tc::tmem_dealloc<kTmemCols>(tmem);
 }
 
+// Key-split partials -> output: per row, weights l_p e^(m_p - M) over the
+// splits in a fixed order (one warp per row, 4 columns per lane).
+__global__ void attn_v5_merge_kernel(const __nv_bfloat16* __restrict__ part_o, const float* __restrict__ part_ml,
+                                     int P, int64_t rows, __nv_bfloat16* __restrict__ out,
+                                     float* __restrict__ ml_out) {
+  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  float M = -INFINITY;
+  for (int p = 0; p < P; ++p) M = fmaxf(M, part_ml[2 * (p * rows + r)]);
+  float L = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int p = 0; p < P; ++p) {
+    const float m = part_ml[2 * (p * rows + r)];
+    const float w = m == -INFINITY ? 0.f : part_ml[2 * (p * rows + r) + 1] * __expf(m - M);
+    L += w;
+    const uint2 u = *reinterpret_cast<const uint2*>(part_o + (p * rows + r) * kDh + lane * 4);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+    const float2 c = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+    acc[0] += w * a.x;
+    acc[1] += w * a.y;
+    acc[2] += w * c.x;
+    acc[3] += w * c.y;
+  }
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  uint2 o;
+  o.x = tc::pack_bf16(acc[0] * inv, acc[1] * inv);
+  o.y = tc::pack_bf16(acc[2] * inv, acc[3] * inv);
+  *reinterpret_cast<uint2*>(out + r * kDh + lane * 4) = o;
+  if (ml_out && lane == 0) {
+    ml_out[2 * r] = M;
+    ml_out[2 * r + 1] = L;
+  }
+}
+
 }  // namespace
 }  // namespace ifkv
 
@@ -552,8 +589,34 @@ extern "C" int ifkv_recompute_attn_tc_v5(const void* q, const void* k_layer, con
   const int per_pair = 2 * (kRows / Gp);
   const int pairs = (S + per_pair - 1) / per_pair;
   const float scale_log2 = scale * 1.4426950408889634f;
-  recompute_attn_v5_kernel<<<dim3(Hkv, pairs, 1), 384, smem, as_stream(stream)>>>(
-      tq, tk, tv, horizon, S, H, Hkv, Gp, scale_log2, (__nv_bfloat16*)out, ml_out);
-  IFKV_LAUNCH_CHECK("recompute_attn_v5");
+  cudaStream_t st = as_stream(stream);
+  // key splits (gridDim.z) when the tile pairs alone leave the GPU under two
+  // waves: the heaviest (latest) pairs are split first into equal key ranges
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int P = 1;
+#if IFKV_ATTN5_SPLITS
+  if (Hkv * pairs < 2 * sms) P = min(4, (2 * sms + Hkv * pairs - 1) / (Hkv * pairs));
+#endif
+  if (P == 1) {
+    recompute_attn_v5_kernel<<<dim3(Hkv, pairs, 1), 384, smem, st>>>(tq, tk, tv, horizon, S, H, Hkv, Gp,
+                                                                     scale_log2, (__nv_bfloat16*)out, ml_out);
+    IFKV_LAUNCH_CHECK("recompute_attn_v5");
+    return IFKV_OK;
+  }
+  const int64_t rows = (int64_t)S * H;
+  void* ws = nullptr;
+  const size_t o_bytes = (size_t)P * rows * kDh * 2, ml_bytes = (size_t)P * rows * 2 * 4;
+  IFKV_CUDA_CALL(cudaMallocAsync(&ws, o_bytes + ml_bytes, st), "recompute_attn_v5: split workspace");
+  auto* part_o = reinterpret_cast<__nv_bfloat16*>(ws);
+  auto* part_ml = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + o_bytes);
+  recompute_attn_v5_kernel<<<dim3(Hkv, pairs, P), 384, smem, st>>>(tq, tk, tv, horizon, S, H, Hkv, Gp, scale_log2,
+                                                                   part_o, part_ml);
+  IFKV_LAUNCH_CHECK("recompute_attn_v5 (split)");
+  attn_v5_merge_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(part_o, part_ml, P, rows, (__nv_bfloat16*)out,
+                                                                     ml_out);
+  IFKV_LAUNCH_CHECK("recompute_attn_v5 (merge)");
+  IFKV_CUDA_CALL(cudaFreeAsync(ws, st), "recompute_attn_v5: free split workspace");
   return IFKV_OK;
 }
