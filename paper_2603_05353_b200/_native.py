@@ -9,12 +9,14 @@ IFKV_ERR_CUDA -> NativeError, each with the library's thread-local message.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
 from .errors import ConfigurationError, NativeError
 
-LIB_PATH = Path(__file__).resolve().parent / "_build" / "libifkv.so"
+# IFKV_LIB: load an A/B build (tools/build_variants.py -> _ab/<name>/libifkv.so) instead
+LIB_PATH = Path(os.environ.get("IFKV_LIB", Path(__file__).resolve().parent / "_build" / "libifkv.so"))
 
 IFKV_F32, IFKV_BF16 = 0, 1
 OUT_F32, OUT_BF16, OUT_SPLIT3 = 0, 1, 2
