@@ -248,6 +248,7 @@ def run_ours(args, world, rank, local):
     attn = prof.get("recompute_attn", [])
     attn_ms = [a.elapsed_time(b) for a, b, _ in attn]
     sct = [(a.elapsed_time(b), w) for a, b, w in prof.get("qkv_rope_scatter", [])]
+    pmm = [(a.elapsed_time(b), w) for a, b, w in prof.get("prompt_mm", [])]
     rot = prof.get("rotate_rows", [])
     rot_ms = [a.elapsed_time(b) for a, b, _ in rot]
     del res
@@ -324,6 +325,16 @@ def run_ours(args, world, rank, local):
                     "algorithmic_bytes_per_launch": b_s, "launches_per_step": len(sct),
                     "traffic": ncu_traffic("qkv_rope_scatter")}
 
+    pmm_roof = None
+    if pmm:  # scoring-pass weight-stream GEMMs (bytes: weights + activation terms read, split partials written)
+        t_p, b_p = sum(t for t, _ in pmm), sum(w for _, w in pmm)
+        ach = b_p / (t_p / 1e3) / 1e9
+        pmm_roof = {"kernel": "ifkv prompt_mm (tcgen05 weight stream)", "bound": "hbm", "achieved": ach,
+                    "peak": PEAKS["hbm_gbs"], "unit": "GB/s", "frac": ach / PEAKS["hbm_gbs"],
+                    "ms_per_step": t_p, "algorithmic_bytes_per_step": b_p, "launches_per_step": len(pmm),
+                    "traffic": ncu_traffic("prompt_mm"),
+                    "traffic_note": "ncu DRAM bytes of one launch (layer-0 gate|up, 235 MB of weights)"}
+
     # comparator: full bf16 prefill of the same context through the same kernels
     torch.cuda.synchronize()
     ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -358,6 +369,7 @@ def run_ours(args, world, rank, local):
         "roofline": roof,
         "roofline_kernel1": rot_roof,
         "roofline_scatter": sct_roof,
+        "roofline_prompt_mm": pmm_roof,
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clk,

@@ -287,7 +287,8 @@ def mm_parts(x, w):
         n = w.shape[1]
         s = prompt_mm_splits(n, k, rows, _sm_count(), p)
         out = torch.empty((s, rows, n), dtype=torch.float32, device=x.device)
-        N.call("ifkv_prompt_mm", N.ptr(x), p, rows, k, N.ptr(w), n, s, N.ptr(out), _s())
+        with _Bracket("prompt_mm", k * n * 2 + p * rows * k * 2 + s * rows * n * 4):  # W + X read, partials written
+            N.call("ifkv_prompt_mm", N.ptr(x), p, rows, k, N.ptr(w), n, s, N.ptr(out), _s())
         return out
     if x.dim() == 3:
         p, rows, k = x.shape
