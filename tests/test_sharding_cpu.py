@@ -3,7 +3,6 @@ cross-rank merges run over torch.distributed `gloo` with world size 2,
 checked against unsharded oracle computations."""
 
 import os
-import socket
 
 import numpy as np
 import pytest
@@ -43,19 +42,11 @@ def test_local_horizon_is_visible_prefix():
         assert l == int((grows <= h).sum()) - 1
 
 
-def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    return port
-
-
-def _worker(rank, world, port, fn, q):
+def _worker(rank, world, store_path, fn, q):
     import torch.distributed as dist
 
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # a FileStore rendezvous: no TCP port to race for between test runs
+    dist.init_process_group("gloo", init_method=f"file://{store_path}", rank=rank, world_size=world)
     try:
         q.put((rank, fn(SH.TorchComm())))
     except Exception as exc:  # pragma: no cover - surfaced in the parent
@@ -65,17 +56,20 @@ def _worker(rank, world, port, fn, q):
 
 
 def _run_gloo(fn, world=2):
+    import tempfile
+
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, fn, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    out = dict(q.get(timeout=120) for _ in range(world))
-    for p in procs:
-        p.join(timeout=60)
+    with tempfile.TemporaryDirectory() as tmp:
+        store = os.path.join(tmp, "store")
+        procs = [ctx.Process(target=_worker, args=(r, world, store, fn, q)) for r in range(world)]
+        for p in procs:
+            p.start()
+        out = dict(q.get(timeout=120) for _ in range(world))
+        for p in procs:
+            p.join(timeout=60)
     for v in out.values():
         if isinstance(v, Exception):
             raise v
