@@ -120,9 +120,12 @@ def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or os.environ.get("IFKV_FORCE_SHARDED"):
         import torch.distributed as dist
 
+        # IFKV_FORCE_SHARDED=1 runs the chunk-sharded path even at world 1
+        # (a one-rank NCCL communicator: every collective of the N-GPU bench
+        # path on the one GPU this environment reaches).
         # IFKV_DIST_BACKEND=gloo runs the same TorchComm data path with every
         # rank on the visible GPUs round-robin (a functional check of the
         # multi-process path on a one-GPU box); the default is NCCL, one GPU per rank.
@@ -587,7 +590,7 @@ def main():
             print(json.dumps(line), flush=True)
         return
     world, rank, local = dist_setup()
-    if world > 1:
+    if world > 1 or os.environ.get("IFKV_FORCE_SHARDED"):
         from paper_2603_05353_b200.sharding import TorchComm
 
         import torch.distributed as dist

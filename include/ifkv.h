@@ -204,6 +204,13 @@ int ifkv_recompute_attn_simt(int dtype, const void* q, const void* k_layer, cons
  * local context (0 when no key is visible), ml_out [S][H][2] = (max, sum exp)
  * -- for the cross-rank merge.  horizon[i] may be -1 (no local key <= the
  * query's global index). */
+/* Merge P partial attentions of the same queries over disjoint key sets (the
+ * chunk-sharded recompute, recompute.py:114 over every rank's keys): part_o
+ * bf16 [P][rows][Dh] each normalised by its own sum, part_ml fp32
+ * [P][rows][2] = (max in natural-log units, sum); out bf16 [rows][Dh],
+ * optional ml_out [rows][2].  Fixed p order (deterministic). */
+int ifkv_merge_partials(const void* part_o, const float* part_ml, int P, int64_t rows, int Dh, void* out,
+                        float* ml_out, void* stream);
 int ifkv_recompute_attn_partial(int dtype, const void* q, const void* k_layer, const void* v_layer,
                                 const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows, float scale,
                                 void* out, float* ml_out, void* stream);

@@ -227,6 +227,17 @@ def recompute_attn_partial(q, k_layer, v_layer, horizon, H, Hkv, Dh):
     return out, ml
 
 
+def merge_partials(parts_o, parts_ml):
+    """parts_o bf16 [P, S, H, Dh] (each normalised), parts_ml fp32 [P, S, H, 2]
+    -> merged bf16 [S, H, Dh] (ifkv_merge_partials, fixed part order)."""
+    torch = _torch()
+    P, S, H, Dh = parts_o.shape
+    out = torch.empty((S, H, Dh), dtype=parts_o.dtype, device=parts_o.device)
+    N.call("ifkv_merge_partials", N.ptr(parts_o.contiguous()), N.ptr(parts_ml.contiguous()), P, S * H, Dh, N.ptr(out),
+           None, _s())
+    return out
+
+
 def recompute_attn(q, k_layer, v_layer, horizon, H, Hkv, Dh, out=None, impl: str = "auto"):
     """impl: "auto" (tcgen05 when supported, else SIMT) or "simt"."""
     torch = _torch()

@@ -295,3 +295,22 @@ def test_prompt_mm_weight_stream_gemm(T, cuda, P, R, K, N):
 
     with pytest.raises(ConfigurationError):
         NV.call("ifkv_prompt_mm", NV.ptr(x), P, 16, K, NV.ptr(w), N, 1, NV.ptr(out), NV.stream_handle())
+
+
+def test_merge_partials_matches_state_merge(T, cuda):
+    """ifkv_merge_partials (the chunk-sharded recompute's per-layer merge)
+    against the torch softmax-state merge, including keyless partials."""
+    from paper_2603_05353_b200 import engine as E
+    from paper_2603_05353_b200 import sharding as SH
+
+    g = T.Generator(device="cuda").manual_seed(3)
+    P, S, H, Dh = 3, 37, 4, 128
+    o = T.randn(P, S, H, Dh, device="cuda", generator=g).to(T.bfloat16)
+    m = T.randn(P, S, H, device="cuda", generator=g) * 4
+    l = T.rand(P, S, H, device="cuda", generator=g) * 10 + 0.1
+    m[1, :5] = -float("inf")  # rank 1 saw no key for these queries
+    l[1, :5] = 0.0
+    ml = T.stack([m, l], dim=-1)
+    got = E.merge_partials(o, ml).float()
+    want = SH.merge_query_states(list(o), list(ml)).float()
+    assert float((got - want).abs().max() / want.abs().max()) < 1e-2
