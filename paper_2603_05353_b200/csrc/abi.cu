@@ -1,6 +1,8 @@
 // ABI bookkeeping: thread-local error message and version.
 #include <stdarg.h>
 
+#include <mutex>
+
 #include "common.cuh"
 
 namespace ifkv {
@@ -11,6 +13,21 @@ void set_error(const char* fmt, ...) {
   va_start(ap, fmt);
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
+}
+
+void* workspace_alloc(size_t bytes, cudaStream_t st) {
+  static std::once_flag once[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::call_once(once[dev & 63], [dev] {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;  // never trim at synchronize: split workspaces are reused per query
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  });
+  void* p = nullptr;
+  return cudaMallocAsync(&p, bytes, st) == cudaSuccess ? p : nullptr;
 }
 }  // namespace ifkv
 

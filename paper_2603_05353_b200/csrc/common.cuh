@@ -41,6 +41,14 @@ void set_error(const char* fmt, ...);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Stream-ordered workspace (cudaMallocAsync) for the attention key splits.
+// The device's default memory pool returns freed memory to the driver at
+// every synchronize (release threshold 0), so the first split launch after
+// each query's host sync re-mapped its workspace -- tens of ms in a step
+// (C4 at 5 % recompute).  Keep it in the pool instead.
+void* workspace_alloc(size_t bytes, cudaStream_t st);
+
+
 __device__ __forceinline__ float to_f32(float x) { return x; }
 __device__ __forceinline__ float to_f32(__nv_bfloat16 x) { return __bfloat162float(x); }
 

@@ -130,17 +130,7 @@ static int recompute_attn_tc_any(const void* q, const void* k_layer, const void*
                                  int S, int H, int Hkv, int Dh, int n_rows, float scale, void* out, float* ml_out,
                                  void* stream) {
   int gen = IFKV_ATTN_GEN;
-  if (gen == 0) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int Gp = 1;  // v5 pads the GQA group to a power of two (zero query rows)
-    while (Hkv > 0 && Gp < H / Hkv) Gp *= 2;
-    const int per_pair = 2 * (128 / Gp);
-    const int64_t pairs = ((int64_t)S + per_pair - 1) / per_pair;
-    const bool padded = Hkv > 0 && Gp != H / Hkv;  // v5 computes zero rows for G < Gp
-    gen = (!padded || (int64_t)Hkv * pairs >= 2 * sms) ? 5 : 4;
-  }
+  if (gen == 0) gen = 5;
   if (gen == 5)
     return ifkv_recompute_attn_tc_v5(q, k_layer, v_layer, horizon, S, H, Hkv, Dh, n_rows, scale, out, ml_out,
                                      stream);

@@ -575,7 +575,11 @@ extern "C" int ifkv_recompute_attn_tc(const void* q, const void* k_layer, const 
   const int64_t rows = (int64_t)S * H;
   void* ws = nullptr;
   const size_t o_bytes = (size_t)P * rows * kDh * 2, ml_bytes = (size_t)P * rows * 2 * 4;
-  IFKV_CUDA_CALL(cudaMallocAsync(&ws, o_bytes + ml_bytes, st), "recompute_attn_tc: split workspace");
+  ws = workspace_alloc(o_bytes + ml_bytes, st);
+  if (!ws) {
+    set_error("recompute_attn_tc: split workspace (%zu bytes)", o_bytes + ml_bytes);
+    return IFKV_ERR_CUDA;
+  }
   auto* part_o = reinterpret_cast<__nv_bfloat16*>(ws);
   auto* part_ml = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + o_bytes);
   recompute_attn_tc_kernel<<<dim3(Hkv, pairs, P), 384, smem, st>>>(tq, tk, tv, horizon, S, H, Hkv, scale_log2,

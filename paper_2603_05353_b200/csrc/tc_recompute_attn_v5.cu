@@ -38,6 +38,9 @@ constexpr float kRescaleLog2 = 8.0f;
 #ifndef IFKV_ATTN5_SPLITS
 #define IFKV_ATTN5_SPLITS 1
 #endif
+#ifndef IFKV_ATTN5_EXACTG
+#define IFKV_ATTN5_EXACTG 1
+#endif
 
 struct Smem {
   uint8_t q[2][kTile];
@@ -86,7 +89,7 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
   // tile row = token (row / Gp) x head of the group (row % Gp); Gp is G rounded
   // up to a power of two -- the padded heads are zero query rows (TMA OOB fill)
   const int tok = t0 + row / Gp;
-  const bool valid = row % Gp < G && tok < S;
+  const bool valid = row < (kRows / Gp) * Gp && row % Gp < G && tok < S;  // tile rows: tokens x Gp heads
   const int hz = valid ? (int)horizon[tok] : INT_MAX;  // pad rows: never force the masked path
   const uint32_t lane_off = (uint32_t)(w * 32) << 16;
   const uint32_t t_s = tmem + 256 * x + lane_off;
@@ -329,6 +332,17 @@ __global__ void __launch_bounds__(384, 1)
     }
     tc::fence_barrier_init();
   }
+  {
+    // a group that does not divide 128 rows (G = 7: 18 tokens x 7 heads =
+    // 126 rows) leaves the last rows of each Q tile outside the TMA box: zero
+    // them (generic-proxy stores, made visible to the tensor core below)
+    const int tile_rows = tok * Gp;
+    for (int i = threadIdx.x; i < 2 * 2 * (kRows - tile_rows) * 8; i += blockDim.x) {
+      const int c = i & 7, r = tile_rows + ((i >> 3) % (kRows - tile_rows)), pq = (i >> 3) / (kRows - tile_rows);
+      *reinterpret_cast<uint4*>(sm.q[pq >> 1] + (pq & 1) * kPanel + r * 128 + c * 16) = make_uint4(0, 0, 0, 0);
+    }
+    tc::fence_async_smem();
+  }
   if (warp == 2) tc::tmem_alloc<kTmemCols>(&sm.tmem_base);
   tc::tc_fence_before();
   __syncthreads();
@@ -347,7 +361,7 @@ __global__ void __launch_bounds__(384, 1)
       tc::tma_prefetch(&tm_q);
       tc::tma_prefetch(&tm_k);
       tc::tma_prefetch(&tm_v);
-      tc::mbar_arrive_expect_tx(&sm.q_full, (nB > 0 ? 2 : 1) * kTile);  // box = tok x Gp = 128 rows
+      tc::mbar_arrive_expect_tx(&sm.q_full, (nB > 0 ? 2 : 1) * 2 * tok * Gp * 128);  // box = tok x Gp rows
       tc::tma_load_4d(sm.q[0], &tm_q, &sm.q_full, 0, 0, g, tA);
       tc::tma_load_4d(sm.q[0] + kPanel, &tm_q, &sm.q_full, 64, 0, g, tA);
       if (nB > 0) {
@@ -561,12 +575,15 @@ extern "C" int ifkv_recompute_attn_tc_v5(const void* q, const void* k_layer, con
   IFKV_CHECK_ARG(Dh == kDh && Hkv > 0 && H % Hkv == 0 && H / Hkv <= 16, "recompute_attn_v5: unsupported shape");
   if (S <= 0) return IFKV_OK;
   const int G = H / Hkv;
+  // heads per tile row group: G itself (tiles of floor(128/G) tokens x G heads,
+  // the last 128 mod G rows zero), or G padded to a power of two (A/B)
   int Gp = 1;
-  while (Gp < G) Gp *= 2;  // heads per tile row group, padded to a power of two
+  while (Gp < G) Gp *= 2;
+  if (IFKV_ATTN5_EXACTG) Gp = G;
   CUtensorMap tq, tk, tv;
   {
-    // q [S][Hkv][G][Dh] viewed 4-D; the box takes Gp >= G heads: rows of
-    // heads G..Gp-1 fall outside the tensor and are zero-filled by TMA
+    // q [S][Hkv][G][Dh] viewed 4-D; the box takes Gp >= G heads (padded
+    // variant: rows of heads G..Gp-1 fall outside the tensor, zero-filled by TMA)
     uint64_t dims[4] = {(uint64_t)Dh, (uint64_t)G, (uint64_t)Hkv, (uint64_t)S};
     uint64_t strides[3] = {(uint64_t)Dh * 2, (uint64_t)G * Dh * 2, (uint64_t)H * Dh * 2};
     uint32_t box[4] = {64, (uint32_t)Gp, 1, (uint32_t)(kRows / Gp)};
@@ -608,7 +625,11 @@ extern "C" int ifkv_recompute_attn_tc_v5(const void* q, const void* k_layer, con
   const int64_t rows = (int64_t)S * H;
   void* ws = nullptr;
   const size_t o_bytes = (size_t)P * rows * kDh * 2, ml_bytes = (size_t)P * rows * 2 * 4;
-  IFKV_CUDA_CALL(cudaMallocAsync(&ws, o_bytes + ml_bytes, st), "recompute_attn_v5: split workspace");
+  ws = workspace_alloc(o_bytes + ml_bytes, st);
+  if (!ws) {
+    set_error("recompute_attn_v5: split workspace (%zu bytes)", o_bytes + ml_bytes);
+    return IFKV_ERR_CUDA;
+  }
   auto* part_o = reinterpret_cast<__nv_bfloat16*>(ws);
   auto* part_ml = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + o_bytes);
   recompute_attn_v5_kernel<<<dim3(Hkv, pairs, P), 384, smem, st>>>(tq, tk, tv, horizon, S, H, Hkv, Gp, scale_log2,
