@@ -114,15 +114,15 @@ extern "C" int ifkv_recompute_attn_tc_v4(const void* q, const void* k_layer, con
 extern "C" int ifkv_recompute_attn_tc_v5(const void* q, const void* k_layer, const void* v_layer,
                                          const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows,
                                          float scale, void* out, float* ml_out, void* stream);
-// tcgen05 kernel generation: v5 (two ping-ponging tiles per CTA, P staged in
-// smem so S(j+1) follows the read of S(j); 3-5 % faster than v2, identical
-// results; GQA groups padded to a power of two; key splits below two waves),
-// except for a padded group (G = 7: 1/8 of v5's rows are zeros) on a grid
-// under two waves, where v4 (one tile per CTA, triple-buffered S, column-split
-// softmax, key splits) is 2.5 % faster.  v5 vs v4 at G = 4 (ms per layer,
-// C2 shape): k = 1639 0.445-0.48 vs 0.47-0.52, k = 2458 0.57-0.64 vs
-// 0.64-0.74, k = 3277 0.79-0.94 vs 0.84-0.98, k = 4916 1.07-1.20 vs 1.23-1.42
-// (profiles/r1_attn_ab.md).  IFKV_ATTN_GEN=2/4/5 pins one (A/B).
+// tcgen05 kernel generation: v5 for every grid (two ping-ponging tiles per
+// CTA, P staged in smem so S(j+1) follows the read of S(j); tiles of
+// floor(128/G) tokens x G heads; key splits below two waves).  Measured
+// against v4 (one tile per CTA, triple-buffered S, column-split softmax):
+// G = 4, ms per layer at the C2 shape: k = 1639 0.445-0.48 vs 0.47-0.52,
+// k = 2458 0.57-0.64 vs 0.64-0.74, k = 3277 0.79-0.94 vs 0.84-0.98, k = 4916
+// 1.07-1.20 vs 1.23-1.42; G = 7: k = 1639 0.38-0.40 vs 0.41-0.43, k = 4916
+// 0.94-1.05 vs 1.07-1.26 (profiles/r1_attn_ab.md).  IFKV_ATTN_GEN=2/4/5 pins
+// one generation (A/B).
 #ifndef IFKV_ATTN_GEN
 #define IFKV_ATTN_GEN 0
 #endif
