@@ -211,6 +211,12 @@ int ifkv_recompute_attn_simt(int dtype, const void* q, const void* k_layer, cons
  * optional ml_out [rows][2].  Fixed p order (deterministic). */
 int ifkv_merge_partials(const void* part_o, const float* part_ml, int P, int64_t rows, int Dh, void* out,
                         float* ml_out, void* stream);
+/* The same merge for the scoring pass's per-layer prompt states (chunk
+ * sharding, selection.py:127-169 over every rank's keys): part_ctx fp32
+ * [P][G][M][H][Dh], part_ml fp32 [P][G][H][M][2] -> out_ctx [G][M][H][Dh],
+ * out_ml [G][H][M][2]. */
+int ifkv_merge_prompt_states(const float* part_ctx, const float* part_ml, int P, int G, int M, int H, int Dh,
+                             float* out_ctx, float* out_ml, void* stream);
 int ifkv_recompute_attn_partial(int dtype, const void* q, const void* k_layer, const void* v_layer,
                                 const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows, float scale,
                                 void* out, float* ml_out, void* stream);

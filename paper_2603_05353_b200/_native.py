@@ -50,6 +50,7 @@ SIGNATURES = {
     "ifkv_recompute_attn_tc_supported": [I32, I32, I32, I32],
     "ifkv_recompute_attn_partial": [I32, P, P, P, P, I32, I32, I32, I32, I32, F32, P, P, P],
     "ifkv_merge_partials": [P, P, I32, I64, I32, P, P, P],
+    "ifkv_merge_prompt_states": [P, P, I32, I32, I32, I32, I32, P, P, P],
 }
 EXPORTS = tuple(SIGNATURES) + ("ifkv_last_error", "ifkv_abi_version")
 

@@ -179,52 +179,51 @@ extern "C" int ifkv_recompute_attn(int dtype, const void* q, const void* k_layer
 }
 
 namespace ifkv {
-// Softmax-state merge of P partial attentions (chunk sharding: every rank's
-// keys for the same queries; recompute.py:114 over the union of the keys):
-// out[r] = sum_p l_p e^(m_p - M) o_p / sum_p l_p e^(m_p - M), fixed p order.
-// One warp per row; part_o bf16 [P][rows][Dh] (each normalised by its own
-// l), part_ml fp32 [P][rows][2] = (m in natural-log units, l).
-__global__ void merge_partials_kernel(const __nv_bfloat16* __restrict__ part_o, const float* __restrict__ part_ml,
-                                      int P, int64_t rows, int Dh, __nv_bfloat16* __restrict__ out,
-                                      float* __restrict__ ml_out) {
+// Softmax-state merge of P partial attentions of the same queries over
+// disjoint key sets (chunk sharding: recompute.py:114 and model.py:297-315
+// over every rank's keys):
+//   out[r] = sum_p l_p e^(m_p - M) o_p / sum_p l_p e^(m_p - M), fixed p order.
+// One warp per context row r (Dh columns, 4 per lane per 128); parts_o
+// [P][rows][Dh] each normalised by its own l.  The (m, l) pairs may be laid
+// out in another row order: context row r = (g, m, h) of [G][M][H] reads ml
+// row (g, h, m) of [G][H][M] (the prompt states); M = 1 makes them the same
+// order (the query states).  m in natural-log units.
+template <typename TC>
+__global__ void merge_states_kernel(const TC* __restrict__ part_o, const float* __restrict__ part_ml, int P,
+                                    int64_t rows, int Dh, int H, int M, TC* __restrict__ out,
+                                    float* __restrict__ ml_out) {
   const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
-  float M = -INFINITY;
-  for (int p = 0; p < P; ++p) M = fmaxf(M, part_ml[2 * (p * rows + r)]);
+  const int64_t g = r / ((int64_t)M * H), mi = (r / H) % M, h = r % H;
+  const int64_t rm = (g * H + h) * M + mi;
+  float Mx = -INFINITY;
+  for (int p = 0; p < P; ++p) Mx = fmaxf(Mx, part_ml[2 * (p * rows + rm)]);
   float L = 0.f;
   for (int c0 = 0; c0 < Dh; c0 += 128) {
     const int c = c0 + lane * 4;
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     float Lc = 0.f;
     for (int p = 0; p < P; ++p) {
-      const float m = part_ml[2 * (p * rows + r)];
-      const float w = m == -INFINITY ? 0.f : part_ml[2 * (p * rows + r) + 1] * __expf(m - M);
+      const float m = part_ml[2 * (p * rows + rm)];
+      const float w = m == -INFINITY ? 0.f : part_ml[2 * (p * rows + rm) + 1] * expf(m - Mx);
       Lc += w;
       if (c < Dh) {
-        const uint2 u = *reinterpret_cast<const uint2*>(part_o + (p * rows + r) * Dh + c);
-        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
-        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
-        acc[0] += w * a.x;
-        acc[1] += w * a.y;
-        acc[2] += w * b.x;
-        acc[3] += w * b.y;
+        const TC* src = part_o + (p * rows + r) * Dh + c;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] += w * to_f32(src[u]);
       }
     }
     L = Lc;
     if (c < Dh) {
       const float inv = L > 0.f ? 1.f / L : 0.f;
-      __nv_bfloat162 x = __floats2bfloat162_rn(acc[0] * inv, acc[1] * inv);
-      __nv_bfloat162 y = __floats2bfloat162_rn(acc[2] * inv, acc[3] * inv);
-      uint2 o;
-      o.x = *reinterpret_cast<uint32_t*>(&x);
-      o.y = *reinterpret_cast<uint32_t*>(&y);
-      *reinterpret_cast<uint2*>(out + r * Dh + c) = o;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) out[r * Dh + c + u] = from_f32<TC>(acc[u] * inv);
     }
   }
   if (ml_out && lane == 0) {
-    ml_out[2 * r] = M;
-    ml_out[2 * r + 1] = L;
+    ml_out[2 * rm] = Mx;
+    ml_out[2 * rm + 1] = L;
   }
 }
 }  // namespace ifkv
@@ -233,9 +232,20 @@ extern "C" int ifkv_merge_partials(const void* part_o, const float* part_ml, int
                                    float* ml_out, void* stream) {
   IFKV_CHECK_ARG(P >= 1 && rows >= 0 && Dh > 0 && Dh % 4 == 0, "merge_partials: bad shape");
   if (rows == 0) return IFKV_OK;
-  merge_partials_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, as_stream(stream)>>>(
-      (const __nv_bfloat16*)part_o, part_ml, P, rows, Dh, (__nv_bfloat16*)out, ml_out);
+  merge_states_kernel<__nv_bfloat16><<<(unsigned)((rows + 7) / 8), 256, 0, as_stream(stream)>>>(
+      (const __nv_bfloat16*)part_o, part_ml, P, rows, Dh, 1, 1, (__nv_bfloat16*)out, ml_out);
   IFKV_LAUNCH_CHECK("merge_partials");
+  return IFKV_OK;
+}
+
+extern "C" int ifkv_merge_prompt_states(const float* part_ctx, const float* part_ml, int P, int G, int M, int H,
+                                        int Dh, float* out_ctx, float* out_ml, void* stream) {
+  IFKV_CHECK_ARG(P >= 1 && G >= 0 && M > 0 && H > 0 && Dh > 0 && Dh % 4 == 0, "merge_prompt_states: bad shape");
+  const int64_t rows = (int64_t)G * M * H;
+  if (rows == 0) return IFKV_OK;
+  merge_states_kernel<float><<<(unsigned)((rows + 7) / 8), 256, 0, as_stream(stream)>>>(
+      part_ctx, part_ml, P, rows, Dh, H, M, out_ctx, out_ml);
+  IFKV_LAUNCH_CHECK("merge_prompt_states");
   return IFKV_OK;
 }
 

@@ -238,6 +238,18 @@ def merge_partials(parts_o, parts_ml):
     return out
 
 
+def merge_prompt_states(parts_ctx, parts_ml):
+    """parts_ctx fp32 [P, G, M, H, Dh], parts_ml fp32 [P, G, H, M, 2] -> merged
+    (ctx [G, M, H, Dh], ml [G, H, M, 2]) (ifkv_merge_prompt_states)."""
+    torch = _torch()
+    P, G, M, H, Dh = parts_ctx.shape
+    ctx = torch.empty(parts_ctx.shape[1:], dtype=torch.float32, device=parts_ctx.device)
+    ml = torch.empty(parts_ml.shape[1:], dtype=torch.float32, device=parts_ctx.device)
+    N.call("ifkv_merge_prompt_states", N.ptr(parts_ctx.contiguous()), N.ptr(parts_ml.contiguous()), P, G, M, H, Dh,
+           N.ptr(ctx), N.ptr(ml), _s())
+    return ctx, ml
+
+
 def recompute_attn(q, k_layer, v_layer, horizon, H, Hkv, Dh, out=None, impl: str = "auto"):
     """impl: "auto" (tcgen05 when supported, else SIMT) or "simt"."""
     torch = _torch()

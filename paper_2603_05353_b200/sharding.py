@@ -293,6 +293,10 @@ def sharded_select(weights, shard: Shard, cache: AssembledCache, prompt_token_id
     group = E.PromptGroup(prompt, prompt_pos, E.segments_from_deltas(shard.global_rows - cache.row_positions[:n_local]))
 
     def hook(ctx, ml):
+        if comm.world == 1:
+            return ctx, ml
+        if ctx.is_cuda and ctx.dtype == torch.float32:  # one fused merge kernel per layer
+            return E.merge_prompt_states(torch.stack(comm.all_gather(ctx)), torch.stack(comm.all_gather(ml)))
         return merge_prompt_states(comm.all_gather(ctx), comm.all_gather(ml))
 
     out = E.prompt_forward(weights, cache.keys, cache.values, [group], capture_layer=nl, merge_hook=hook,

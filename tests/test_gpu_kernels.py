@@ -314,3 +314,23 @@ def test_merge_partials_matches_state_merge(T, cuda):
     got = E.merge_partials(o, ml).float()
     want = SH.merge_query_states(list(o), list(ml)).float()
     assert float((got - want).abs().max() / want.abs().max()) < 1e-2
+
+
+def test_merge_prompt_states_matches_state_merge(T, cuda):
+    """ifkv_merge_prompt_states (the chunk-sharded scoring pass's per-layer
+    merge) against the torch merge, including ranks that saw no key."""
+    from paper_2603_05353_b200 import engine as E
+    from paper_2603_05353_b200 import sharding as SH
+
+    g = T.Generator(device="cuda").manual_seed(4)
+    P, G, M, H, Dh = 3, 2, 32, 8, 128
+    ctx = T.randn(P, G, M, H, Dh, device="cuda", generator=g)
+    m = T.randn(P, G, H, M, device="cuda", generator=g) * 3
+    l = T.rand(P, G, H, M, device="cuda", generator=g) * 5 + 0.1
+    m[2, :, :3] = -float("inf")
+    l[2, :, :3] = 0.0
+    ml = T.stack([m, l], dim=-1)
+    got_c, got_ml = E.merge_prompt_states(ctx, ml)
+    want_c, want_ml = SH.merge_prompt_states(list(ctx), list(ml))
+    assert float((got_c - want_c).abs().max() / want_c.abs().max()) < 1e-5
+    assert T.allclose(got_ml, want_ml, rtol=1e-5, atol=0)
