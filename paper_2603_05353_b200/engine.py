@@ -547,7 +547,7 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
 
 
 def layer_stack(weights, token_ids, positions, k_slab, v_slab, dst_rows, horizon, want_hidden: bool = False,
-                attn_fn=None, n_layers: Optional[int] = None, on_hidden=None):
+                attn_fn=None, n_layers: Optional[int] = None, on_hidden=None, fused_residual: Optional[bool] = None):
     """Advance S tokens (device int64 ids/positions) through every layer
     (or the first ``n_layers``).
 
@@ -571,9 +571,12 @@ def layer_stack(weights, token_ids, positions, k_slab, v_slab, dst_rows, horizon
     if not 1 <= run <= cfg.n_layers:
         raise ConfigurationError(f"n_layers {run} outside [1, {cfg.n_layers}]")
     # h complete after every layer when the residual adds run in the GEMM
-    # epilogue.  The chunk-sharded path (attn_fn) keeps the separate add: its
-    # ranks-as-threads mode hung inside concurrent torch.addmm(out=...) calls.
-    fused = (FUSED_RESIDUAL and attn_fn is None) or on_hidden is not None
+    # epilogue.  With ranks as threads of one process (sharding.ThreadComm) the
+    # caller keeps the separate add (concurrent torch.addmm(out=...) from
+    # several threads is avoided there); one process per GPU fuses it.
+    if fused_residual is None:
+        fused_residual = attn_fn is None
+    fused = (FUSED_RESIDUAL and fused_residual) or on_hidden is not None
     cs = rope_table(positions, Dh, cfg.rope_base, dev)
     h = embed_rows(weights.embedding, token_ids)
     qbuf = torch.empty((S, H, Dh), dtype=weights.torch_dtype, device=dev)
