@@ -72,6 +72,28 @@ class Comm:
     def all_to_all(self, parts: list, recv_sizes=None) -> list:
         return list(parts)
 
+    def all_gather_var_async(self, t, sizes):
+        """Start all_gather_var; ``.wait()`` on the handle returns the list.
+        Lets the caller compute on its own data while the gather is in flight."""
+        return _Done(self.all_gather_var(t, sizes))
+
+
+class _Done:
+    def __init__(self, value):
+        self.value = value
+
+    def wait(self):
+        return self.value
+
+
+class _Pending:
+    def __init__(self, work, bufs, sizes, keep):
+        self.work, self.bufs, self.sizes, self.keep = work, bufs, sizes, keep
+
+    def wait(self):
+        self.work.wait()  # NCCL: the current stream waits for the collective's stream
+        return [x[:n] for x, n in zip(self.bufs, self.sizes)]
+
 
 class TorchComm(Comm):
     """torch.distributed collectives (NCCL for CUDA tensors, gloo for CPU)."""
@@ -102,6 +124,15 @@ class TorchComm(Comm):
         pad = t.new_zeros((cap,) + tuple(t.shape[1:]))
         pad[: t.shape[0]] = t
         return [x[:n] for x, n in zip(self.all_gather(pad), sizes)]
+
+    def all_gather_var_async(self, t, sizes):
+        t = t.contiguous()
+        cap = max(sizes) if sizes else 0
+        pad = t.new_zeros((cap,) + tuple(t.shape[1:]))
+        pad[: t.shape[0]] = t
+        bufs = [pad.new_empty(pad.shape) for _ in range(self.world)]
+        work = self.dist.all_gather(bufs, pad, group=self.group, async_op=True)
+        return _Pending(work, bufs, sizes, pad)
 
     def all_to_all(self, parts, recv_sizes=None):
         parts = [p.contiguous() for p in parts]
@@ -341,17 +372,34 @@ def sharded_recompute(weights, shard: Shard, cache: AssembledCache, selected_glo
     # collectives below need no host round trip (the GPU never drains)
     hz_parts = comm.all_gather_var(sel_g)
     sizes = [int(h.numel()) for h in hz_parts]
-    hz_local = torch.searchsorted(grows, torch.cat(hz_parts), right=True) - 1
+    hz_loc = [torch.searchsorted(grows, hp, right=True) - 1 for hp in hz_parts]  # local causal horizons
+    hz_mine = hz_loc[comm.rank]
+    others = [r for r in range(comm.world) if r != comm.rank]
+    hz_rem = torch.cat([hz_loc[r] for r in others]) if others else hz_mine[:0]
     mine_n = [sizes[comm.rank]] * comm.world
 
     def attn_fn(li, q_local, k_layer, v_layer):
-        q_all = torch.cat(comm.all_gather_var(q_local, sizes))
-        ctx, ml = E.recompute_attn_partial(q_all, k_layer, v_layer, hz_local, H, Hkv, Dh)
+        # this rank's queries against its keys while the other ranks' queries
+        # are gathered (NCCL runs the gather on its own stream), then theirs
+        pending = comm.all_gather_var_async(q_local, sizes)
+        ctx_l, ml_l = E.recompute_attn_partial(q_local, k_layer, v_layer, hz_mine, H, Hkv, Dh)
         if comm.world == 1:  # one shard: the partial is the whole attention
-            return ctx
-        back_ctx = comm.all_to_all(list(torch.split(ctx, sizes)), mine_n)
-        back_ml = comm.all_to_all(list(torch.split(ml, sizes)), mine_n)
-        if ctx.dtype == torch.bfloat16:  # one fused merge kernel instead of ~10 elementwise passes
+            return ctx_l
+        parts = pending.wait()
+        q_rem = torch.cat([parts[r] for r in others])
+        ctx_r, ml_r = E.recompute_attn_partial(q_rem, k_layer, v_layer, hz_rem, H, Hkv, Dh)
+        send_ctx, send_ml, off = [], [], 0
+        for r in range(comm.world):
+            if r == comm.rank:
+                send_ctx.append(ctx_l)
+                send_ml.append(ml_l)
+            else:
+                send_ctx.append(ctx_r[off: off + sizes[r]])
+                send_ml.append(ml_r[off: off + sizes[r]])
+                off += sizes[r]
+        back_ctx = comm.all_to_all(send_ctx, mine_n)
+        back_ml = comm.all_to_all(send_ml, mine_n)
+        if q_local.dtype == torch.bfloat16:  # one fused merge kernel instead of ~10 elementwise passes
             return E.merge_partials(torch.stack(back_ctx), torch.stack(back_ml))
         return merge_query_states(back_ctx, back_ml).to(q_local.dtype)
 
