@@ -13,7 +13,8 @@ size-independent properties the reference's own tests pin
   (test_recompute.py:76-83); positions / provenance of the replaced rows;
 * the whole path is deterministic (bit-identical on a second run);
 * ratio 1.0 equals a full prefill of the same context (test_recompute.py:33-39);
-* the chunk-sharded path (2 ranks simulated on the GPU) selects the same set.
+* the chunk-sharded path (2 ranks simulated on the GPU) selects the same set;
+* reorder (C3 at 32K): permutation, importances, permuted cache, second pass.
 Random-init weights (the reference's distribution), as in bench.py."""
 
 import math
@@ -133,3 +134,34 @@ def test_c2_sharded_two_ranks_select_the_same_set(c2):
 
     for got in SH.ThreadComm.run(2, body):
         np.testing.assert_array_equal(got, want)
+
+
+def test_c3_reorder_properties(c2):
+    """Information-flow reorder at full size (reorder.py:57-181, test_reorder.py):
+    the permutation is the stable argsort of the importances (most important
+    last), each importance is the sum of its chunk's first-pass top-k scores,
+    the permuted cache holds the chunks' KV in that order, and the second pass
+    is the exact top-k of its scores under the permuted GLOBAL layout."""
+    P, cfg, w, gen, kvs = c2
+    import torch
+
+    k = math.ceil(RATIO * N_CTX)
+    plan, cache, second = P.reorder_and_reselect(w, gen.chunks, gen.prompt_token_ids, k, prefilled=kvs)
+    imp = np.asarray(plan.chunk_importance, np.float64)
+    np.testing.assert_array_equal(plan.permutation, np.argsort(imp, kind="stable"))
+    per_chunk = math.ceil(k / len(gen.chunks))
+    for ci, fp in enumerate(plan.first_pass):
+        s = fp.scores.double().cpu().numpy()
+        sel = fp.selected_numpy()
+        assert sel.size == min(per_chunk, s.size)
+        np.testing.assert_array_equal(np.sort(sel), np.sort(np.argsort(-s.astype(np.float32), kind="stable")[:sel.size]))
+        assert abs(s[sel].sum() - imp[ci]) <= 1e-6 * max(1.0, abs(imp[ci]))
+    row = 0
+    for ci in plan.permutation:  # the permuted cache: chunk KVs in the new order, bit-exact
+        n = kvs[ci].length
+        assert torch.equal(cache.values[:, row:row + n], kvs[ci].values)
+        row += n
+    s2 = second.scores.float().cpu().numpy()
+    got = second.selected_numpy()
+    assert got.size == k
+    np.testing.assert_array_equal(got, np.sort(np.argsort(-s2, kind="stable")[:k]))
