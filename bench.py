@@ -405,10 +405,15 @@ def run_sharded(args, comm, world, rank, sync):
     sel_cfg = P.SelectionConfig(ratio=args.ratio)
     n_ctx = sum(c.local_length for c in chunks)
 
+    budget = sel_cfg.resolve_budget(n_ctx)
+
     def step(prompt_ids):
-        local = P.assemble(my_kvs)
-        res = SH.sharded_select(weights, shard, local, prompt_ids, sel_cfg, comm)
-        SH.sharded_recompute(weights, shard, local, res.selected, comm)
+        if args.reorder:  # first pass per rank, permutation from the all-gathered importances
+            _, _, pshard, local = SH.sharded_reorder(weights, chunks, my_kvs, shard, prompt_ids, budget, comm)
+        else:
+            pshard, local = shard, P.assemble(my_kvs)
+        res = SH.sharded_select(weights, pshard, local, prompt_ids, sel_cfg, comm)
+        SH.sharded_recompute(weights, pshard, local, res.selected, comm)
         return res
 
     from paper_2603_05353_b200 import _native as N
@@ -457,8 +462,10 @@ def run_sharded(args, comm, world, rank, sync):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (reference generate_task uniform_noise tokens; random-init weights)",
-        "config": {"workload": f"C2 chunk-sharded over {world} ranks (zig-zag chunk ownership, NCCL softmax-state "
-                               f"merges + top-k candidate all-gather + sparse-query partial attention all-to-all)",
+        "config": {"workload": f"{'C3' if args.reorder else 'C2'} chunk-sharded over {world} ranks (zig-zag chunk "
+                               f"ownership, {'per-rank reorder first pass + importance all-gather, ' if args.reorder else ''}"
+                               f"NCCL softmax-state merges + top-k candidate all-gather + sparse-query partial "
+                               f"attention all-to-all)",
                    "ctx_tokens": n_ctx, "chunks": len(chunks), "recompute_ratio": args.ratio,
                    "selected": int(sel_host.size), "parallelism": f"chunk-sharded x{world}",
                    "l2": "inputs larger than L2"},

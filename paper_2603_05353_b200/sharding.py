@@ -348,6 +348,47 @@ def sharded_select(weights, shard: Shard, cache: AssembledCache, prompt_token_id
     return SelectionResult(scores=scores, selected=sel, strategy="attention-norm", geometry="GLOBAL")
 
 
+def sharded_reorder(weights, chunks: Sequence, chunk_kvs: Sequence, shard: Shard, prompt_token_ids, budget: int,
+                    comm: Comm, norm_layer: Optional[int] = None, chunk_score: str = "sum"):
+    """Information-flow reordering over chunk shards (reorder.py:57-181, SURVEY
+    §8e item 4).  The first pass is per chunk and needs no exchange: each rank
+    scores its own chunks (``chunk_kvs``: this rank's KVs, in ``shard.chunk_ids``
+    order); the importances are all-gathered and every rank computes the same
+    stable permutation.  Chunks stay on their ranks: the permuted layout only
+    changes their global rows.  Returns (permutation, importances, the shard in
+    the permuted layout, this rank's cache assembled in that layout's order)."""
+    torch = _torch()
+    from .cache import assemble
+    from .reorder import score_chunks
+
+    n_total = sum(c.local_length for c in chunks)
+    mine = [chunks[c] for c in shard.chunk_ids]
+    if mine:
+        imp_local, _ = score_chunks(weights, mine, prompt_token_ids, budget, norm_layer=norm_layer,
+                                    chunk_score=chunk_score, prefilled=list(chunk_kvs),
+                                    _context=(len(chunks), n_total))
+    else:
+        imp_local = np.zeros(0, np.float64)
+    dev = weights.device
+    ids = comm.all_gather_var(torch.as_tensor(np.asarray(shard.chunk_ids, np.int64), device=dev))
+    imps = comm.all_gather_var(torch.as_tensor(np.asarray(imp_local, np.float64), device=dev))
+    importances = np.zeros(len(chunks), np.float64)
+    for i, v in zip(ids, imps):
+        importances[i.cpu().numpy()] = v.cpu().numpy()
+    permutation = np.argsort(importances, kind="stable").astype(np.int64)  # most important last
+    lens = np.asarray([c.local_length for c in chunks], np.int64)
+    slot_of = np.empty(len(chunks), np.int64)
+    slot_of[permutation] = np.arange(len(chunks))
+    starts = np.concatenate([[0], np.cumsum(lens[permutation])[:-1]])  # global start of each slot
+    order = sorted(range(len(shard.chunk_ids)), key=lambda i: slot_of[shard.chunk_ids[i]])
+    owned = [shard.chunk_ids[i] for i in order]  # ascending in the permuted layout
+    rows = [starts[slot_of[c]] + np.arange(lens[c]) for c in owned]
+    pshard = Shard(shard.rank, shard.world, owned,
+                   np.concatenate(rows).astype(np.int64) if rows else np.zeros(0, np.int64), int(n_total))
+    local = assemble([chunk_kvs[i] for i in order])
+    return permutation, importances, pshard, local
+
+
 def sharded_recompute(weights, shard: Shard, cache: AssembledCache, selected_global, comm: Comm) -> AssembledCache:
     """Recompute the globally selected tokens, each on the rank owning it,
     with attention over every rank's keys; K/V scattered into the owners'

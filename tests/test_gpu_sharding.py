@@ -105,3 +105,45 @@ def test_torchcomm_nccl_single_rank_path(cuda):
         assert rel_err(lk, wk[:, :2048]) <= 1e-2
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_reorder_matches_oracle(cuda, world):
+    """Chunk-sharded information-flow reordering (first pass per rank, the
+    importances all-gathered, one permutation everywhere, chunks kept on
+    their ranks under the permuted global rows) then the sharded GLOBAL
+    selection and recompute: permutation and selected set bit-exact against
+    the oracle's reorder_and_reselect, recomputed K/V within the bf16 bar."""
+    import paper_2603_05353_b200 as P
+    from paper_2603_05353_b200 import sharding as SH
+
+    cfg = P.c1_config()
+    dw = P.DeviceWeights.from_host(P.init_weights(cfg, 7), "bf16")
+    ow = dw.to_host()
+    task = P.SyntheticTask(kind="uniform_noise", total_length=2048, fixed_size=256, prompt_length=32,
+                           vocab_size=1024)
+    g = P.generate_task(task, 3)
+    kvs = [P.prefill_chunk(dw, c) for c in g.chunks]
+    budget = 308
+    perm, _, _, _, sel = O.reorder_and_reselect(ow, [oracle_chunk(c) for c in kvs], g.prompt_token_ids, budget)
+
+    def body(comm):
+        shard = SH.make_shard([c.length for c in kvs], comm.rank, comm.world)
+        mine = [kvs[i] for i in shard.chunk_ids]
+        p, _, pshard, local = SH.sharded_reorder(dw, g.chunks, mine, shard, g.prompt_token_ids, budget, comm)
+        res = SH.sharded_select(dw, pshard, local, g.prompt_token_ids, P.SelectionConfig(topk=budget), comm)
+        SH.sharded_recompute(dw, pshard, local, res.selected, comm)
+        return p, res.selected.cpu().numpy(), pshard, to_np(local.keys)
+
+    outs = SH.ThreadComm.run(world, body)
+    for p, s, pshard, lk in outs:
+        np.testing.assert_array_equal(p, perm)
+        np.testing.assert_array_equal(s, sel)
+    # the recomputed shards together equal the unsharded GPU reorder path's cache (decode layout)
+    plan, cache, second = P.reorder_and_reselect(dw, g.chunks, g.prompt_token_ids, budget, prefilled=kvs)
+    out = P.recompute_selected(dw, cache, P.make_plan(cache, second.selected))
+    want = to_np(out.keys)
+    got = np.zeros_like(want[:, :2048])
+    for _, _, pshard, lk in outs:
+        got[:, pshard.global_rows] = lk[:, : pshard.global_rows.size]
+    assert rel_err(got, want[:, :2048]) <= 1e-2
