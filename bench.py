@@ -71,6 +71,7 @@ def parse():
     ap.add_argument("--reorder", action="store_true", help="information-flow chunk reordering (config 3)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sdpa-comparator", action="store_true", help="skip the torch-SDPA full-prefill comparator")
     ap.add_argument("--ncu", action="store_true", help="one warm step inside cudaProfilerStart/Stop, then exit")
     ap.add_argument("--simulate-ranks", type=int, default=1,
                     help="run the chunk-sharded path with R ranks as threads on one GPU (functional check)")
@@ -206,6 +207,66 @@ def workload_name(args, cfg, n_ctx, n_chunks, k):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+
+
+def sdpa_full_prefill_ms(weights, toks, backend):
+    """The ≤10 % comparator as SURVEY §8d defines it: a full bf16 causal prefill
+    of the same context with torch + library attention (``backend``: a
+    torch.nn.attention.SDPBackend), K/V written per layer; cuBLAS GEMMs.  Returns
+    ms (CUDA events, second of two runs), or None when the backend refuses."""
+    import torch
+    import torch.nn.functional as F
+    from torch.nn.attention import sdpa_kernel
+
+    cfg = weights.config
+    H, Hkv, Dh, d = cfg.n_heads, cfg.kv_heads, cfg.d_head, cfg.d_model
+    n = int(toks.size)
+    ids = torch.as_tensor(toks, device="cuda")
+    pos = torch.arange(n, device="cuda", dtype=torch.float64)
+    inv = cfg.rope_base ** (-torch.arange(0, Dh, 2, device="cuda", dtype=torch.float64) / Dh)
+    ang = pos[:, None] * inv[None, :]
+    cos, sin = ang.cos().float()[:, None, :], ang.sin().float()[:, None, :]
+
+    def rope(x):  # [n, heads, Dh] interleaved pairs, fp32 math
+        xf = x.float().view(n, x.shape[1], Dh // 2, 2)
+        a, b = xf[..., 0], xf[..., 1]
+        return torch.stack([a * cos - b * sin, a * sin + b * cos], dim=-1).view(n, x.shape[1], Dh).to(x.dtype)
+
+    def rms(h, g):
+        return (h * torch.rsqrt(h.pow(2).mean(-1, keepdim=True) + 1e-6) * g).to(torch.bfloat16)
+
+    def run():
+        h = weights.embedding.index_select(0, ids).float()
+        kv = []
+        for lw in weights.layers:
+            qkv = rms(h, lw.attn_norm) @ lw.wqkv
+            q, k, v = qkv.split([H * Dh, Hkv * Dh, Hkv * Dh], dim=-1)
+            q, k = rope(q.view(n, H, Dh)), rope(k.view(n, Hkv, Dh))
+            v = v.view(n, Hkv, Dh)
+            kv.append((k, v))
+            o = F.scaled_dot_product_attention(q.transpose(0, 1)[None], k.transpose(0, 1)[None],
+                                               v.transpose(0, 1)[None], is_causal=True, enable_gqa=True)
+            h = h + (o[0].transpose(0, 1).reshape(n, H * Dh) @ lw.wo).float()
+            gu = rms(h, lw.mlp_norm) @ lw.wgu
+            g, u = gu.split(cfg.d_ff, dim=-1)
+            h = h + ((F.silu(g.float()) * u.float()).to(torch.bfloat16) @ lw.wdown).float()
+        return kv
+
+    try:
+        with sdpa_kernel([backend]):
+            times = []
+            for _ in range(2):
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                out = run()
+                b.record()
+                torch.cuda.synchronize()
+                times.append(a.elapsed_time(b))
+                del out
+        return times[-1]
+    except Exception:  # noqa: BLE001 -- backend not available for this shape/GPU
+        return None
 
 
 def run_ours(args, world, rank, local):
@@ -366,12 +427,25 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize()
     ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     toks = np.concatenate([c.token_ids for c in chunks])
-    ea.record()
-    full = P.full_prefill(weights, toks)
-    eb.record()
-    torch.cuda.synchronize()
-    full_ms = ea.elapsed_time(eb)
-    del full
+    ours_ms = []
+    for _ in range(2):  # the first run also allocates the 32K-row activations
+        torch.cuda.synchronize()
+        ea.record()
+        full = P.full_prefill(weights, toks)
+        eb.record()
+        torch.cuda.synchronize()
+        ours_ms.append(ea.elapsed_time(eb))
+        del full
+    full_by = {"ours (same kernels)": ours_ms[-1]}
+    if not args.no_sdpa_comparator:
+        from torch.nn.attention import SDPBackend
+
+        for name, be in (("torch SDPA cuDNN", SDPBackend.CUDNN_ATTENTION), ("torch SDPA flash", SDPBackend.FLASH_ATTENTION)):
+            t = sdpa_full_prefill_ms(weights, toks, be)
+            if t is not None:
+                full_by[name] = t
+        torch.cuda.empty_cache()
+    full_ms = min(full_by.values())  # best of: the comparator is the fastest full prefill measured
 
     line = {
         "metric": METRIC,
@@ -392,6 +466,7 @@ def run_ours(args, world, rank, local):
                    "l2": "inputs larger than L2 (4.3 GB KV slab + 16 GB weights per step)"},
         "stages_ms": stages,
         "full_prefill_ms": full_ms,
+        "full_prefill_ms_by": full_by,
         "ratio_vs_full_prefill": ms / full_ms,
         "roofline": roof,
         "roofline_kernel1": rot_roof,
