@@ -437,7 +437,7 @@ def run_ours(args, world, rank, local):
         ours_ms.append(ea.elapsed_time(eb))
         del full
     full_by = {"ours (same kernels)": ours_ms[-1]}
-    if not args.no_sdpa_comparator:
+    if not args.no_sdpa_comparator and n_ctx <= 65536:  # (at 128K the torch prefills alone take minutes)
         from torch.nn.attention import SDPBackend
 
         for name, be in (("torch SDPA cuDNN", SDPBackend.CUDNN_ATTENTION), ("torch SDPA flash", SDPBackend.FLASH_ATTENTION)):
