@@ -38,6 +38,13 @@ constexpr float kRescaleLog2 = 8.0f;
 #ifndef IFKV_ATTN5_SPLITS
 #define IFKV_ATTN5_SPLITS 1
 #endif
+// key splits while the tile pairs fill fewer than this many waves (x SMs), up to SPLIT_MAX
+#ifndef IFKV_ATTN5_SPLIT_WAVES
+#define IFKV_ATTN5_SPLIT_WAVES 2
+#endif
+#ifndef IFKV_ATTN5_SPLIT_MAX
+#define IFKV_ATTN5_SPLIT_MAX 4
+#endif
 #ifndef IFKV_ATTN5_EXACTG
 #define IFKV_ATTN5_EXACTG 1
 #endif
@@ -614,7 +621,8 @@ extern "C" int ifkv_recompute_attn_tc_v5(const void* q, const void* k_layer, con
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int P = 1;
 #if IFKV_ATTN5_SPLITS
-  if (Hkv * pairs < 2 * sms) P = min(4, (2 * sms + Hkv * pairs - 1) / (Hkv * pairs));
+  if (Hkv * pairs < IFKV_ATTN5_SPLIT_WAVES * sms)
+    P = min(IFKV_ATTN5_SPLIT_MAX, (IFKV_ATTN5_SPLIT_WAVES * sms + Hkv * pairs - 1) / (Hkv * pairs));
 #endif
   if (P == 1) {
     recompute_attn_v5_kernel<<<dim3(Hkv, pairs, 1), 384, smem, st>>>(tq, tk, tv, horizon, S, H, Hkv, Gp,
