@@ -37,6 +37,15 @@ def test_argument_errors_map_to_configuration_error():
     # rope_table validates before touching the device: d_head must be even
     with pytest.raises(P.ConfigurationError):
         N.call("ifkv_rope_table", None, 4, 7, 10000.0, None, None)
+    # the newer entry points validate their shapes before any CUDA call too
+    with pytest.raises(P.ConfigurationError):  # rows must be a multiple of 32
+        N.call("ifkv_prompt_mm", None, 3, 16, 4096, None, 4096, 1, None, None)
+    with pytest.raises(P.ConfigurationError):  # splits > K / 64
+        N.call("ifkv_prompt_mm", None, 3, 32, 128, None, 4096, 3, None, None)
+    with pytest.raises(P.ConfigurationError):
+        N.call("ifkv_merge_partials", None, None, 0, 10, 128, None, None, None)
+    with pytest.raises(P.ConfigurationError):
+        N.call("ifkv_merge_prompt_states", None, None, 2, 1, 32, 8, 126, None, None, None)
 
 
 def test_model_config_validation():
