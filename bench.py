@@ -219,6 +219,7 @@ def sdpa_full_prefill_ms(weights, toks, backend):
     from torch.nn.attention import sdpa_kernel
 
     cfg = weights.config
+    blk = weights.gu_block
     H, Hkv, Dh, d = cfg.n_heads, cfg.kv_heads, cfg.d_head, cfg.d_model
     n = int(toks.size)
     ids = torch.as_tensor(toks, device="cuda")
@@ -239,17 +240,17 @@ def sdpa_full_prefill_ms(weights, toks, backend):
         h = weights.embedding.index_select(0, ids).float()
         kv = []
         for lw in weights.layers:
-            qkv = rms(h, lw.attn_norm) @ lw.wqkv
+            qkv = rms(h, lw.attn_norm) @ lw.wqkv.t()
             q, k, v = qkv.split([H * Dh, Hkv * Dh, Hkv * Dh], dim=-1)
             q, k = rope(q.view(n, H, Dh)), rope(k.view(n, Hkv, Dh))
             v = v.view(n, Hkv, Dh)
             kv.append((k, v))
             o = F.scaled_dot_product_attention(q.transpose(0, 1)[None], k.transpose(0, 1)[None],
                                                v.transpose(0, 1)[None], is_causal=True, enable_gqa=True)
-            h = h + (o[0].transpose(0, 1).reshape(n, H * Dh) @ lw.wo).float()
-            gu = rms(h, lw.mlp_norm) @ lw.wgu
-            g, u = gu.split(cfg.d_ff, dim=-1)
-            h = h + ((F.silu(g.float()) * u.float()).to(torch.bfloat16) @ lw.wdown).float()
+            h = h + (o[0].transpose(0, 1).reshape(n, H * Dh) @ lw.wo.t()).float()
+            gu = (rms(h, lw.mlp_norm) @ lw.wgu.t()).view(n, -1, 2, blk)  # gate/up interleaved in blk blocks
+            g, u = gu[:, :, 0].reshape(n, cfg.d_ff), gu[:, :, 1].reshape(n, cfg.d_ff)
+            h = h + ((F.silu(g.float()) * u.float()).to(torch.bfloat16) @ lw.wdown.t()).float()
         return kv
 
     try:

@@ -85,10 +85,12 @@ int ifkv_assemble_gather(int dtype, int n_chunks, const void* const* src_k, cons
  * out = rms_norm(h) * gain in out_mode (IFKV_OUT_*).  out may be NULL. */
 int ifkv_add_rmsnorm(float* h, const void* delta, int delta_dtype, int n_parts, const float* gain, int rows,
                      int d, int out_mode, void* out, void* stream);
-/* a = silu(g) * u with gu = [rows][2*d_ff] (gate | up), summed over n_parts
- * part blocks; out in out_mode. */
-int ifkv_silu_mul(const void* gu, int gu_dtype, int n_parts, int rows, int d_ff, int out_mode, void* out,
-                  void* stream);
+/* a = silu(g) * u with gu = [rows][2*d_ff], gate and up columns interleaved
+ * in blocks of gu_block (gate j..j+gu_block-1, then up j.., ...; gu_block =
+ * d_ff is the plain [gate | up] layout), summed over n_parts part blocks;
+ * out in out_mode. */
+int ifkv_silu_mul(const void* gu, int gu_dtype, int n_parts, int rows, int d_ff, int gu_block, int out_mode,
+                  void* out, void* stream);
 /* h[r] = (float) table[ids[r]] (embedding gather, recompute.py:95). */
 int ifkv_embed_rows(const void* table, int dtype, const int64_t* ids, int rows, int d, float* h, void* stream);
 /* out = sum over n_parts of x (fp32 blocks of n elements) -> fp32 or split3. */
@@ -99,12 +101,37 @@ int ifkv_split3(const float* x, int64_t n, void* out, void* stream);
 int ifkv_row_dist_accum(const float* a, const float* b, int rows, int d, double* acc, void* stream);
 /* Prompt-row GEMM of the scoring pass (x @ W of model.py:435-455 for the M
  * prompt rows, selection.py:127-169): out[s][r][n] = sum_{p<P} sum_{k in
- * split s} x[p][r][k] w[k][n]; x bf16 [P][R][K] (the split3 terms), w bf16
- * [K][N] row-major, out fp32 [splits][R][N] (per-split partials, summed by the
+ * split s} x[p][r][k] w[n][k]; x bf16 [P][R][K] (the split3 terms), w bf16
+ * [N][K] ("out x in", W^T of x @ W), out fp32 [splits][R][N] (per-split partials, summed by the
  * consumer's n_parts).  R % 32 == 0, P*R <= 256, K % 64 == 0, N % 128 == 0,
  * 1 <= splits <= K/64.  HBM-bound weight stream on tcgen05 (replaces the
  * cuBLAS calls of the scoring layers). */
 int ifkv_prompt_mm(const void* x, int P, int R, int K, const void* w, int N, int splits, float* out, void* stream);
+
+/* ---- projection GEMMs of the layer stack (tcgen05 CTA pairs) -------------
+ * C[M][N] = A[M][K] . W[N][K]^T: A bf16 activations (row stride lda), W a bf16
+ * weight stored "out x in" (K-major, row stride K).  Replaces the x @ W of
+ * recompute.py:98-116 / model.py:433-455 (cuBLAS in round 1).  tile_n: the
+ * CTA-pair tile as 1000 + BN (256 rows x BN = 256/224/192/160/128 columns),
+ * 0 = chosen by shape.
+ *
+ * ifkv_gemm: out fp32 or bf16 [M][ldo]; accumulate != 0 (fp32 only) adds into
+ * out (h += ctx Wo, h += a Wdown: the residual adds of model.py:448-452). */
+int ifkv_gemm(const void* a, int64_t lda, int M, int K, const void* w, int N, int out_dtype, void* out, int64_t ldo,
+              int accumulate, int tile_n, void* stream);
+/* QKV projection with RoPE and the in-place K/V scatter in the epilogue
+ * (recompute.py:99-112 + replace_entries cache.py:354-363): W rows are
+ * [wq^T; wk^T; wv^T] (Dh = 128), or only [wk^T; wv^T] when kv_only.  q, k
+ * rotated by cs[m] (fp32 (cos, sin) [M][64]); q -> q_out [M][H][128]; k, v ->
+ * k_dst / v_dst rows dst_rows[m] (NULL = m) of [*][Hkv][128] bf16 views. */
+int ifkv_gemm_qkv_rope_scatter(const void* a, int64_t lda, int M, int K, const void* w, int H, int Hkv,
+                               int kv_only, const float* cs, void* q_out, void* k_dst, void* v_dst,
+                               const int64_t* dst_rows, int tile_n, void* stream);
+/* gate|up projection with SwiGLU in the epilogue (model.py:283-294): W rows
+ * interleaved in 64-row blocks (gate j..j+63 | up j..j+63 | ...), 2 d_ff
+ * rows; out[m][j] = silu(g_j) u_j, bf16 [M][d_ff]. */
+int ifkv_gemm_swiglu(const void* a, int64_t lda, int M, int K, const void* w, int d_ff, void* out, int tile_n,
+                     void* stream);
 
 /* ---- fresh q/k/v (model.py:433-437, recompute.py:99-112) ----------------
  * qkv = [rows][(H + 2 Hkv) Dh] (GEMM output, qkv_dtype, n_parts part blocks

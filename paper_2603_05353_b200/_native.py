@@ -31,7 +31,7 @@ SIGNATURES = {
     "ifkv_rotate_rows": [I32, P, P, I64, I32, I32, I32, I32, P, P, P],
     "ifkv_assemble_gather": [I32, I32, P, P, P, P, P, P, P, I64, I32, I32, P],
     "ifkv_add_rmsnorm": [P, P, I32, I32, P, I32, I32, I32, P, P],
-    "ifkv_silu_mul": [P, I32, I32, I32, I32, I32, P, P],
+    "ifkv_silu_mul": [P, I32, I32, I32, I32, I32, I32, P, P],
     "ifkv_embed_rows": [P, I32, P, I32, I32, P, P],
     "ifkv_split3": [P, I64, P, P],
     "ifkv_row_dist_accum": [P, P, I32, I32, P, P],
@@ -51,6 +51,9 @@ SIGNATURES = {
     "ifkv_recompute_attn_partial": [I32, P, P, P, P, I32, I32, I32, I32, I32, F32, P, P, P],
     "ifkv_merge_partials": [P, P, I32, I64, I32, P, P, P],
     "ifkv_merge_prompt_states": [P, P, I32, I32, I32, I32, I32, P, P, P],
+    "ifkv_gemm": [P, I64, I32, I32, P, I32, I32, P, I64, I32, I32, P],
+    "ifkv_gemm_qkv_rope_scatter": [P, I64, I32, I32, P, I32, I32, I32, P, P, P, P, P, I32, P],
+    "ifkv_gemm_swiglu": [P, I64, I32, I32, P, I32, P, I32, P],
 }
 EXPORTS = tuple(SIGNATURES) + ("ifkv_last_error", "ifkv_abi_version")
 

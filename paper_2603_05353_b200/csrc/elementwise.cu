@@ -184,7 +184,7 @@ __device__ __forceinline__ float silu_f(float g) {
 
 // 4-wide vectors over [rows][d_ff] (d_ff % 4 == 0).
 template <typename T>
-__global__ void silu_mul_kernel(const T* __restrict__ gu, int n_parts, int rows, int d_ff, int mode,
+__global__ void silu_mul_kernel(const T* __restrict__ gu, int n_parts, int rows, int d_ff, int blk, int mode,
                                 void* __restrict__ out) {
   const int vpr = d_ff / 4;
   const int64_t nv = (int64_t)rows * vpr;
@@ -192,11 +192,11 @@ __global__ void silu_mul_kernel(const T* __restrict__ gu, int n_parts, int rows,
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nv; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = t / vpr;
     const int c = (int)(t - r * vpr) * 4;
-    const T* base = gu + r * 2 * d_ff + c;
-    float4 g = ld4(base), u = ld4(base + d_ff);
+    const T* base = gu + r * 2 * d_ff + (c / blk) * 2 * blk + c % blk;  // gate; up is blk further
+    float4 g = ld4(base), u = ld4(base + blk);
     for (int q = 1; q < n_parts; ++q) {
       add4(g, ld4(base + q * pstride));
-      add4(u, ld4(base + q * pstride + d_ff));
+      add4(u, ld4(base + q * pstride + blk));
     }
     float4 y = make_float4(silu_f(g.x) * u.x, silu_f(g.y) * u.y, silu_f(g.z) * u.z, silu_f(g.w) * u.w);
     store4_mode(out, mode, (int64_t)rows * d_ff, r * d_ff + c, y);
@@ -209,16 +209,16 @@ __device__ __forceinline__ float silu_fast(float g) { return g * __frcp_rn(1.f +
 
 // bf16 -> bf16 fast path (single part): 8 elements per thread-iteration,
 // 16-byte loads of gate and up, 16-byte store.
-__global__ void silu_mul_bf16x8_kernel(const __nv_bfloat16* __restrict__ gu, int rows, int d_ff,
+__global__ void silu_mul_bf16x8_kernel(const __nv_bfloat16* __restrict__ gu, int rows, int d_ff, int blk,
                                        __nv_bfloat16* __restrict__ out) {
   const int vpr = d_ff / 8;
   const int64_t nv = (int64_t)rows * vpr;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nv; t += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(t / vpr);
     const int c = (int)(t - (int64_t)r * vpr) * 8;
-    const __nv_bfloat16* base = gu + (int64_t)r * 2 * d_ff + c;
+    const __nv_bfloat16* base = gu + (int64_t)r * 2 * d_ff + (c / blk) * 2 * blk + c % blk;
     uint4 gv = *reinterpret_cast<const uint4*>(base);
-    uint4 uv = *reinterpret_cast<const uint4*>(base + d_ff);
+    uint4 uv = *reinterpret_cast<const uint4*>(base + blk);
     const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
     const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&uv);
     uint4 ov;
@@ -244,7 +244,7 @@ __device__ __forceinline__ float tanh_approx(float x) {
 // bf16 -> bf16, one part: one pass (no grid-stride loop), two 8-element
 // vectors per thread with all four 16-byte loads issued first, 32-bit indexing.
 __global__ void __launch_bounds__(256) silu_mul_bf16_fast_kernel(const __nv_bfloat16* __restrict__ gu, int total,
-                                                                 int vpr, __nv_bfloat16* __restrict__ out) {
+                                                                 int vpr, int blk, __nv_bfloat16* __restrict__ out) {
   const int t0 = blockIdx.x * 512 + threadIdx.x;
   uint4 gv[2], uv[2];
   int r[2], c[2];
@@ -254,9 +254,10 @@ __global__ void __launch_bounds__(256) silu_mul_bf16_fast_kernel(const __nv_bflo
     r[u] = t / vpr;
     c[u] = t - r[u] * vpr;
     if (t < total) {
-      const __nv_bfloat16* base = gu + (int64_t)r[u] * 16 * vpr + c[u] * 8;
+      const int e = c[u] * 8;
+      const __nv_bfloat16* base = gu + (int64_t)r[u] * 16 * vpr + (e / blk) * 2 * blk + e % blk;
       gv[u] = *reinterpret_cast<const uint4*>(base);
-      uv[u] = *reinterpret_cast<const uint4*>(base + 8 * vpr);
+      uv[u] = *reinterpret_cast<const uint4*>(base + blk);
     }
   }
 #pragma unroll
@@ -384,9 +385,11 @@ extern "C" int ifkv_add_rmsnorm(float* h, const void* delta, int delta_dtype, in
   return IFKV_OK;
 }
 
-extern "C" int ifkv_silu_mul(const void* gu, int gu_dtype, int n_parts, int rows, int d_ff, int out_mode, void* out,
-                             void* stream) {
+extern "C" int ifkv_silu_mul(const void* gu, int gu_dtype, int n_parts, int rows, int d_ff, int gu_block,
+                             int out_mode, void* out, void* stream) {
   IFKV_CHECK_ARG(rows >= 0 && d_ff > 0 && d_ff % 4 == 0 && n_parts >= 1, "silu_mul: d_ff must be a multiple of 4");
+  IFKV_CHECK_ARG(gu_block > 0 && gu_block % 4 == 0 && d_ff % gu_block == 0,
+                 "silu_mul: gu_block must divide d_ff and be a multiple of 4");
   IFKV_CHECK_ARG(out_mode >= IFKV_OUT_F32 && out_mode <= IFKV_OUT_SPLIT3, "silu_mul: bad out mode");
   int64_t n = (int64_t)rows * d_ff / 4;
   if (n == 0) return IFKV_OK;
@@ -395,21 +398,22 @@ extern "C" int ifkv_silu_mul(const void* gu, int gu_dtype, int n_parts, int rows
 #ifndef IFKV_SILU_FAST
 #define IFKV_SILU_FAST 1
 #endif
-  if (IFKV_SILU_FAST && gu_dtype == IFKV_BF16 && n_parts == 1 && out_mode == IFKV_OUT_BF16 && d_ff % 8 == 0 &&
+  if (IFKV_SILU_FAST && gu_dtype == IFKV_BF16 && n_parts == 1 && out_mode == IFKV_OUT_BF16 && gu_block % 8 == 0 &&
       (int64_t)rows * d_ff / 8 + 512 < (int64_t)INT32_MAX) {
     const int total = (int)((int64_t)rows * d_ff / 8);
     silu_mul_bf16_fast_kernel<<<(unsigned)((total + 511) / 512), 256, 0, as_stream(stream)>>>(
-        (const __nv_bfloat16*)gu, total, d_ff / 8, (__nv_bfloat16*)out);
-  } else if (gu_dtype == IFKV_BF16 && n_parts == 1 && out_mode == IFKV_OUT_BF16 && d_ff % 8 == 0) {
+        (const __nv_bfloat16*)gu, total, d_ff / 8, gu_block, (__nv_bfloat16*)out);
+  } else if (gu_dtype == IFKV_BF16 && n_parts == 1 && out_mode == IFKV_OUT_BF16 && gu_block % 8 == 0) {
     const int64_t nv = (int64_t)rows * d_ff / 8;
     const int64_t w8 = (nv + 255) / 256;
     silu_mul_bf16x8_kernel<<<(unsigned)(w8 < 148 * 16 ? w8 : 148 * 16), 256, 0, as_stream(stream)>>>(
-        (const __nv_bfloat16*)gu, rows, d_ff, (__nv_bfloat16*)out);
+        (const __nv_bfloat16*)gu, rows, d_ff, gu_block, (__nv_bfloat16*)out);
   } else if (gu_dtype == IFKV_BF16)
     silu_mul_kernel<__nv_bfloat16><<<grid, 256, 0, as_stream(stream)>>>((const __nv_bfloat16*)gu, n_parts, rows,
-                                                                       d_ff, out_mode, out);
+                                                                       d_ff, gu_block, out_mode, out);
   else
-    silu_mul_kernel<float><<<grid, 256, 0, as_stream(stream)>>>((const float*)gu, n_parts, rows, d_ff, out_mode, out);
+    silu_mul_kernel<float><<<grid, 256, 0, as_stream(stream)>>>((const float*)gu, n_parts, rows, d_ff, gu_block,
+                                                               out_mode, out);
   IFKV_LAUNCH_CHECK("silu_mul");
   return IFKV_OK;
 }

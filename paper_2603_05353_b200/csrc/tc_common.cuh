@@ -279,6 +279,9 @@ PFN_encodeTiled get_encode_tiled();
 // strides in bytes for dims 1.. (dim 0 is contiguous).
 int make_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
                    const uint32_t* box);
+// any element type / swizzle (TMA stores of the GEMM epilogues)
+int make_tmap(CUtensorMap* map, const void* base, CUtensorMapDataType dtype, int rank, const uint64_t* dims,
+              const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle swizzle);
 
 }  // namespace ifkv
 

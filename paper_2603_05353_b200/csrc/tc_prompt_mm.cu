@@ -1,16 +1,15 @@
 // Prompt-row GEMM of the scoring pass on the tcgen05 tensor cores:
 //   out[s][r][n] = sum_{p < P} sum_{k in split s} X[p][r][k] * W[k][n]
 // X: the P (= 3) bf16 split terms of the fp32 activations of the R (= 32)
-// prompt rows, W: a bf16 projection [K][N] row-major (the reference's x @ W,
-// model.py:435-455).  With R*P <= 256 rows the product is a weight stream:
+// prompt rows, W: a bf16 projection stored "out x in" ([N][K], K-major; the
+// reference's x @ W with W^T stored, model.py:435-455).  With R*P <= 256 rows the product is a weight stream:
 // 2 x 96 FLOP per weight byte, far below the tensor ridge, so the kernel is
 // bound by HBM reading W once (selection.py:127-169 runs it for every layer
 // below the capture layer: 8.3 GB of weights at C2).
 //
 // Transposed tile: D^T[n][p*R + r] = W^T[n][k] . X^T[k][p*R + r], so W is the
-// A operand (M = 128 output columns, MN-major straight from the row-major
-// weight, no transposed copy) and the P*R activation rows are the N of the
-// MMA (K-major).  The split terms are summed in fp32 in the epilogue in a
+// A operand (M = 128 output columns, K-major rows of the stored W^T) and the
+// P*R activation rows are the N of the MMA (K-major).  The split terms are summed in fp32 in the epilogue in a
 // fixed order; K is split over gridDim.y so the grid covers the GPU, each
 // split writing its own fp32 partial (out[s]) -- consumers sum the partials
 // in a fixed order (n_parts), so results are deterministic.
@@ -22,8 +21,7 @@ namespace {
 
 constexpr int kN = 128;      // output columns per CTA (MMA M)
 constexpr int kKStep = 64;   // K per stage (one 128-byte swizzle row of X)
-constexpr int kWPanel = kKStep * 128;  // 64 k-rows x 64 n (128 B) = 8 KB
-constexpr int kWStage = 2 * kWPanel;   // 16 KB: 128 n x 64 k
+constexpr int kWStage = 128 * 128;    // 16 KB: 128 n rows x 64 k (128 B)
 
 template <int kStages>
 __global__ void __launch_bounds__(128, 2)
@@ -65,25 +63,23 @@ __global__ void __launch_bounds__(128, 2)
       tc::mbar_wait(&empty[s], ((i / kStages) & 1) ^ 1);
       uint8_t* st = base + s * stage_bytes;
       tc::mbar_arrive_expect_tx(&full[s], kWStage + x_bytes);
-      tc::tma_load_2d(st, &tm_w, &full[s], n0, k0);
-      tc::tma_load_2d(st + kWPanel, &tm_w, &full[s], n0 + 64, k0);
+      tc::tma_load_2d(st, &tm_w, &full[s], k0, n0);
       tc::tma_load_2d(st + kWStage, &tm_x, &full[s], k0, 0);
     }
   } else if (warp == 1) {
-    // A = W tile, MN-major: 64-wide n groups LBO = 8 KB apart, 8 k-rows per
-    // swizzle atom (SBO 1 KB), K = 16 per MMA = 2 KB down the rows.
-    // B = X tile, K-major: rows of 128 B (64 k), 8-row atoms 1 KB apart.
-    const uint32_t idesc = tc::idesc_bf16(kN, NR, 1, 0);
+    // A = W tile, B = X tile, both K-major: rows of 128 B (64 k), 8-row
+    // swizzle atoms 1 KB apart, K = 16 per MMA = 32 B along the row.
+    const uint32_t idesc = tc::idesc_bf16(kN, NR, 0, 0);
     for (int i = 0; i < ns; ++i) {
       const int s = i % kStages;
       tc::mbar_wait(&full[s], (i / kStages) & 1);
       tc::tc_fence_after();
       const uint32_t st = tc::smem_u32(base + s * stage_bytes);
-      const uint64_t a = tc::smem_desc_sw128(st, kWPanel, 1024);
+      const uint64_t a = tc::smem_desc_sw128(st, 16, 1024);
       const uint64_t b = tc::smem_desc_sw128(st + kWStage, 16, 1024);
 #pragma unroll
       for (int t = 0; t < kKStep / 16; ++t)
-        tc::mma_bf16_ss_ws(tmem, a + (uint64_t)(t * (2048 >> 4)), b + (uint64_t)(t * 2), idesc,
+        tc::mma_bf16_ss_ws(tmem, a + (uint64_t)(t * 2), b + (uint64_t)(t * 2), idesc,
                            (i > 0 || t > 0) ? 1u : 0u);
       tc::mma_commit_ws(&empty[s]);
     }
@@ -120,7 +116,7 @@ __global__ void __launch_bounds__(128, 2)
 
 using namespace ifkv;
 
-// x: bf16 [P][R][K] (contiguous), w: bf16 [K][N] row-major, out: fp32
+// x: bf16 [P][R][K] (contiguous), w: bf16 [N][K] ("out x in"), out: fp32
 // [splits][R][N] (each K split's partial; the caller sums them).
 extern "C" int ifkv_prompt_mm(const void* x, int P, int R, int K, const void* w, int N, int splits, float* out,
                               void* stream) {
@@ -133,9 +129,9 @@ extern "C" int ifkv_prompt_mm(const void* x, int P, int R, int K, const void* w,
   const int NR = P * R;  // MMA N
   CUtensorMap tw, tx;
   {
-    uint64_t dims[2] = {(uint64_t)N, (uint64_t)K};
-    uint64_t strides[1] = {(uint64_t)N * 2};
-    uint32_t box[2] = {64, (uint32_t)kKStep};
+    uint64_t dims[2] = {(uint64_t)K, (uint64_t)N};
+    uint64_t strides[1] = {(uint64_t)K * 2};
+    uint32_t box[2] = {(uint32_t)kKStep, (uint32_t)kN};
     int rc = make_tmap_bf16(&tw, w, 2, dims, strides, box);
     if (rc) return rc;
   }

@@ -11,9 +11,10 @@ path is built from.
   scattered into a slab in place before the layer's attention reads it
   (recompute.py:67-122; the same loop prefills chunks, cache.py:74-99).
 
-PyTorch is plumbing here: tensors own HBM, the current stream orders work,
-cuBLAS (torch.mm) runs the plain projection GEMMs.  Everything else is an
-sm_100a kernel behind include/ifkv.h.
+PyTorch is plumbing here: tensors own HBM and the current stream orders
+work.  Every bf16 step is an sm_100a kernel behind include/ifkv.h (the
+projection GEMMs included: csrc/tc_gemm.cu); only the fp32 parity mode's
+GEMMs use torch.mm.
 """
 
 from __future__ import annotations
@@ -160,13 +161,14 @@ def residual_add(h, delta, n_parts: int):
            N.OUT_F32, None, _s())
 
 
-def silu_mul(gu, n_parts: int, d_ff: int, out_mode: int):
+def silu_mul(gu, n_parts: int, d_ff: int, out_mode: int, gu_block: int):
+    """gu [n_parts, rows, 2 d_ff] (gate/up interleaved in gu_block blocks)."""
     torch = _torch()
     rows = gu.shape[-2]
     shape = (3, rows, d_ff) if out_mode == N.OUT_SPLIT3 else (rows, d_ff)
     dt = torch.float32 if out_mode == N.OUT_F32 else torch.bfloat16
     out = torch.empty(shape, dtype=dt, device=gu.device)
-    N.call("ifkv_silu_mul", N.ptr(gu), dt_code(gu), n_parts, rows, d_ff, out_mode, N.ptr(out), _s())
+    N.call("ifkv_silu_mul", N.ptr(gu), dt_code(gu), n_parts, rows, d_ff, gu_block, out_mode, N.ptr(out), _s())
     return out
 
 
@@ -294,20 +296,67 @@ def prompt_mm_ok(x, w) -> bool:
     if not (PROMPT_MM and x.dim() == 3 and x.dtype == torch.bfloat16 and w.dtype == torch.bfloat16):
         return False
     p, rows, k = x.shape
-    return (rows % 32 == 0 and p * rows <= 256 and k % 64 == 0 and w.shape[0] == k and w.shape[1] % 128 == 0
+    return (rows % 32 == 0 and p * rows <= 256 and k % 64 == 0 and w.shape[1] == k and w.shape[0] % 128 == 0
             and x.is_contiguous() and w.is_contiguous())
 
 
+# Projection GEMMs (C = A W^T, weights stored "out x in"): bf16 operands run
+# on the tcgen05 CTA-pair GEMM (ifkv_gemm*, csrc/tc_gemm.cu) with the
+# consumer fused into its epilogue; fp32 operands (the fp32 parity mode) use
+# torch.mm.  IFKV_GEMM_TILE overrides the tile choice (A/B: 1000 + BN).
+GEMM_TILE = int(os.environ.get("IFKV_GEMM_TILE", "0"))
+
+
+def _gemm_flops(m, k, n):
+    return 2 * m * k * n
+
+
+def gemm(a, w, out_dtype=None, out=None, accumulate: bool = False):
+    """a [M, K] @ w[N, K]^T -> [M, N] (bf16 or fp32); accumulate adds into
+    ``out`` (fp32).  fp32 operands go through torch.mm."""
+    torch = _torch()
+    M, K = a.shape
+    n = w.shape[0]
+    if a.dtype == torch.float32:
+        if accumulate:
+            out.addmm_(a, w.t())
+            return out
+        return torch.mm(a, w.t(), out=out) if out is not None else torch.mm(a, w.t())
+    if out is None:
+        out = torch.empty((M, n), dtype=out_dtype or torch.bfloat16, device=a.device)
+    with _Bracket("gemm", _gemm_flops(M, K, n)):
+        N.call("ifkv_gemm", N.ptr(a), a.stride(0), M, K, N.ptr(w), n, dt_code(out), N.ptr(out), out.stride(0),
+               1 if accumulate else 0, GEMM_TILE, _s())
+    return out
+
+
+def gemm_qkv_rope_scatter(x, w, H, Hkv, cs, q_out, k_dst, v_dst, dst_rows, kv_only: bool = False):
+    M, K = x.shape
+    with _Bracket("gemm", _gemm_flops(M, K, w.shape[0])):
+        N.call("ifkv_gemm_qkv_rope_scatter", N.ptr(x), x.stride(0), M, K, N.ptr(w), H, Hkv, 1 if kv_only else 0,
+               N.ptr(cs), N.ptr(q_out), N.ptr(k_dst), N.ptr(v_dst), N.ptr(dst_rows), GEMM_TILE, _s())
+
+
+def gemm_swiglu(x, w, d_ff):
+    torch = _torch()
+    M, K = x.shape
+    out = torch.empty((M, d_ff), dtype=torch.bfloat16, device=x.device)
+    with _Bracket("gemm", _gemm_flops(M, K, 2 * d_ff)):
+        N.call("ifkv_gemm_swiglu", N.ptr(x), x.stride(0), M, K, N.ptr(w), d_ff, N.ptr(out), GEMM_TILE, _s())
+    return out
+
+
 def mm_parts(x, w):
-    """x: [P, rows, K] (bf16 split terms) or [rows, K] fp32; returns fp32
-    [n, rows, N] part blocks whose sum is x @ w (consumers sum the n blocks):
-    exact products, fp32 sums.  Prompt-row shapes run on ifkv_prompt_mm
-    (n = its K splits, the P terms summed in its epilogue), others on cuBLAS
-    (n = P)."""
+    """x: [P, rows, K] (bf16 split terms) or [rows, K] fp32; w [N, K];
+    returns fp32 [n, rows, N] part blocks whose sum is x @ w^T (consumers sum
+    the n blocks): exact products, fp32 sums.  Prompt-row shapes run on
+    ifkv_prompt_mm (n = its K splits, the P terms summed in its epilogue),
+    larger bf16 ones (the reorder first pass: K groups x 32 rows) on the
+    tcgen05 GEMM with an fp32 output (n = P), fp32 ones on torch."""
     torch = _torch()
     if prompt_mm_ok(x, w):
         p, rows, k = x.shape
-        n = w.shape[1]
+        n = w.shape[0]
         s = prompt_mm_splits(n, k, rows, _sm_count(), p)
         out = torch.empty((s, rows, n), dtype=torch.float32, device=x.device)
         with _Bracket("prompt_mm", k * n * 2 + p * rows * k * 2 + s * rows * n * 4):  # W + X read, partials written
@@ -315,31 +364,9 @@ def mm_parts(x, w):
         return out
     if x.dim() == 3:
         p, rows, k = x.shape
-        y = torch.mm(x.reshape(p * rows, k), w, out_dtype=torch.float32)
-        return y.view(p, rows, w.shape[1])
-    return torch.mm(x, w).unsqueeze(0)
-
-
-# Residual adds of the layer stack inside the O-proj / down-proj GEMMs
-# (cuBLAS epilogue with the fp32 residual stream as C, beta = 1) instead of
-# an fp32 GEMM output re-read by add_rmsnorm.  IFKV_FUSED_RESIDUAL=0 restores
-# the separate add (A/B).
-FUSED_RESIDUAL = os.environ.get("IFKV_FUSED_RESIDUAL", "1") != "0"
-
-
-def mm_f32(a, w):
-    """a @ w with an fp32 result (bf16 operands accumulate in fp32)."""
-    torch = _torch()
-    return torch.mm(a, w, out_dtype=torch.float32) if a.dtype != torch.float32 else torch.mm(a, w)
-
-
-def residual_mm(h, a, w):
-    """h += a @ w in place, fp32 h, fp32 accumulation."""
-    torch = _torch()
-    if a.dtype == torch.float32:
-        h.addmm_(a, w)
-    else:
-        torch.addmm(h, a, w, out_dtype=torch.float32, out=h)
+        y = gemm(x.reshape(p * rows, k), w, out_dtype=torch.float32)
+        return y.view(p, rows, w.shape[0])
+    return torch.mm(x, w.t()).unsqueeze(0)
 
 
 # ---------------------------------------------------------------------------
@@ -531,7 +558,7 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
         o = mm_parts(cx, lw.wo)
         x2 = add_rmsnorm(h, o, o.shape[0], lw.mlp_norm, mode)
         gu = mm_parts(x2, lw.wgu)
-        a = silu_mul(gu, gu.shape[0], cfg.d_ff, mode)
+        a = silu_mul(gu, gu.shape[0], cfg.d_ff, mode, weights.gu_block)
         pending = mm_parts(a, lw.wdown)
         pending_parts = pending.shape[0]
     if want_logits:
@@ -547,7 +574,7 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
 
 
 def layer_stack(weights, token_ids, positions, k_slab, v_slab, dst_rows, horizon, want_hidden: bool = False,
-                attn_fn=None, n_layers: Optional[int] = None, on_hidden=None, fused_residual: Optional[bool] = None):
+                attn_fn=None, n_layers: Optional[int] = None, on_hidden=None):
     """Advance S tokens (device int64 ids/positions) through every layer
     (or the first ``n_layers``).
 
@@ -557,6 +584,11 @@ def layer_stack(weights, token_ids, positions, k_slab, v_slab, dst_rows, horizon
     after its K/V (nothing else can change a K/V row) unless the hidden state
     is wanted; ``on_hidden(l, h)`` sees each layer's block output (fp32 [S, d],
     model.py:450-452).
+
+    bf16 weights: four tcgen05 GEMM launches per layer with fused epilogues
+    (QKV -> RoPE + in-place K/V scatter; h += ctx Wo; gate|up -> SwiGLU;
+    h += a Wdown), plus RMSNorm and the attention.  fp32 weights (parity
+    mode): torch.mm GEMMs with the same elementwise kernels.
     """
     torch = _torch()
     cfg = weights.config
@@ -570,48 +602,39 @@ def layer_stack(weights, token_ids, positions, k_slab, v_slab, dst_rows, horizon
     run = cfg.n_layers if n_layers is None else int(n_layers)
     if not 1 <= run <= cfg.n_layers:
         raise ConfigurationError(f"n_layers {run} outside [1, {cfg.n_layers}]")
-    # h complete after every layer when the residual adds run in the GEMM
-    # epilogue.  With ranks as threads of one process (sharding.ThreadComm) the
-    # caller keeps the separate add (concurrent torch.addmm(out=...) from
-    # several threads is avoided there); one process per GPU fuses it.
-    if fused_residual is None:
-        fused_residual = attn_fn is None
-    fused = (FUSED_RESIDUAL and fused_residual) or on_hidden is not None
+    fused_qkv = bf16 and Dh == 128
+    fused_mlp = bf16 and weights.gu_block == 64
     cs = rope_table(positions, Dh, cfg.rope_base, dev)
     h = embed_rows(weights.embedding, token_ids)
     qbuf = torch.empty((S, H, Dh), dtype=weights.torch_dtype, device=dev)
     attn_out = torch.empty_like(qbuf)
-    pending = None
     for li in range(run):
         lw = weights.layers[li]
         final = li == cfg.n_layers - 1 and not want_hidden and on_hidden is None
-        x = add_rmsnorm(h, pending, 1, lw.attn_norm, act_mode)
-        if final:  # the last layer only contributes K/V: project k, v only
-            kv = torch.mm(x, lw.wqkv[:, H * Dh:])
-            with _Bracket("qkv_rope_scatter", S * 2 * Hkv * Dh * 2 * kv.element_size()):
-                qkv_rope_scatter(kv, 1, 0, Hkv, Dh, cs, None, k_slab[li], v_slab[li], dst_rows)
+        x = add_rmsnorm(h, None, 0, lw.attn_norm, act_mode)
+        wkv = lw.wqkv[H * Dh:] if final else lw.wqkv  # the last layer only contributes K/V
+        if fused_qkv:
+            gemm_qkv_rope_scatter(x, wkv, H, Hkv, cs, None if final else qbuf, k_slab[li], v_slab[li], dst_rows,
+                                  kv_only=final)
+        else:
+            qkv = gemm(x, wkv)
+            with _Bracket("qkv_rope_scatter", S * wkv.shape[0] * 2 * qkv.element_size()):
+                qkv_rope_scatter(qkv, 1, 0 if final else H, Hkv, Dh, cs, None if final else qbuf, k_slab[li],
+                                 v_slab[li], dst_rows)
+        if final:
             return None
-        qkv = torch.mm(x, lw.wqkv)
-        with _Bracket("qkv_rope_scatter", S * (2 * Hkv * Dh + H * Dh) * 2 * qkv.element_size()):
-            qkv_rope_scatter(qkv, 1, H, Hkv, Dh, cs, qbuf, k_slab[li], v_slab[li], dst_rows)
         if attn_fn is not None:  # chunk-sharded: attention over every rank's keys
             attn_out = attn_fn(li, qbuf, k_slab[li], v_slab[li])
         else:
             with _Bracket("recompute_attn", li):
                 recompute_attn(qbuf, k_slab[li], v_slab[li], horizon, H, Hkv, Dh, out=attn_out)
-        if fused:  # h += attn Wo inside the GEMM (fp32 C operand, beta = 1)
-            residual_mm(h, attn_out.view(S, d), lw.wo)
-            x2 = add_rmsnorm(h, None, 0, lw.mlp_norm, act_mode)
+        gemm(attn_out.view(S, d), lw.wo, out=h, accumulate=True)  # h += ctx Wo
+        x2 = add_rmsnorm(h, None, 0, lw.mlp_norm, act_mode)
+        if fused_mlp:
+            a = gemm_swiglu(x2, lw.wgu, cfg.d_ff)
         else:
-            x2 = add_rmsnorm(h, mm_f32(attn_out.view(S, d), lw.wo), 1, lw.mlp_norm, act_mode)
-        gu = torch.mm(x2, lw.wgu)
-        a = silu_mul(gu, 1, cfg.d_ff, act_mode)
-        if fused:
-            residual_mm(h, a, lw.wdown)
-            if on_hidden is not None:
-                on_hidden(li, h)
-        else:
-            pending = mm_f32(a, lw.wdown)
-    if pending is not None:
-        residual_add(h, pending, 1)
+            a = silu_mul(gemm(x2, lw.wgu).unsqueeze(0), 1, cfg.d_ff, act_mode, weights.gu_block)
+        gemm(a, lw.wdown, out=h, accumulate=True)  # h += a Wdown
+        if on_hidden is not None:
+            on_hidden(li, h)
     return h

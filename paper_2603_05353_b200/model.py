@@ -6,10 +6,14 @@ reference is MHA-only, the benchmark shapes (Llama-3-8B, Qwen2.5-VL-7B) are
 GQA.  With ``n_kv_heads`` unset the draw order and shapes are exactly the
 reference's, so ``init_weights`` reproduces its tensors bit for bit.
 
-``DeviceWeights`` is the HBM layout the kernels read: per layer one fused
-[d, (H + 2 Hkv) Dh] QKV matrix, the O projection, one fused [d, 2 d_ff]
-gate|up matrix and the down projection, all row-major (x @ W as in the
-reference), in bf16 (perf) or fp32 (parity mode); norm gains stay fp32.
+``DeviceWeights`` is the HBM layout the kernels read: every projection is
+stored "out x in" (W^T of the reference's x @ W, row-major [N][K]) so both
+GEMM operands are K-major for the tcgen05 kernels: per layer one fused
+[(H + 2 Hkv) Dh, d] QKV matrix, the O projection [d, d], one fused
+[2 d_ff, d] gate|up matrix whose rows interleave gate and up in blocks of
+``gu_block`` (64: gate j..j+63, up j..j+63, ... -- the SwiGLU epilogue pairs
+g_j with u_j inside one tile) and the down projection [d, d_ff]; bf16 (perf)
+or fp32 (parity mode); norm gains stay fp32.
 """
 
 from __future__ import annotations
@@ -219,14 +223,40 @@ def init_weights(config: ModelConfig, seed: int, precision: str = "f64") -> Weig
 # ---------------------------------------------------------------------------
 
 
+def gu_block_for(d_ff: int) -> int:
+    """Gate/up interleave block of the fused gate|up weight: 64 when it
+    divides d_ff (the SwiGLU GEMM epilogue's unit), else d_ff ([gate; up])."""
+    return 64 if d_ff % 64 == 0 else d_ff
+
+
+def interleave_gu(gate_t, up_t, block: int):
+    """[d_ff, d] gate^T and up^T -> [2 d_ff, d] rows (gate block, up block)*.
+    Works for numpy arrays and torch tensors."""
+    dff, d = gate_t.shape
+    nb = dff // block
+    if hasattr(gate_t, "new_empty"):  # torch
+        import torch
+
+        return torch.stack([gate_t.reshape(nb, block, d), up_t.reshape(nb, block, d)], 1).reshape(2 * dff, d)
+    return np.stack([gate_t.reshape(nb, block, d), up_t.reshape(nb, block, d)], 1).reshape(2 * dff, d)
+
+
+def deinterleave_gu(gu_t, block: int):
+    """Inverse of interleave_gu: -> (gate^T, up^T)."""
+    two_dff, d = gu_t.shape
+    dff = two_dff // 2
+    v = gu_t.reshape(dff // block, 2, block, d)
+    return v[:, 0].reshape(dff, d), v[:, 1].reshape(dff, d)
+
+
 @dataclass
 class DeviceLayer:
     attn_norm: "object"  # torch fp32 [d]
-    wqkv: "object"  # [d, (H + 2 Hkv) Dh]
-    wo: "object"  # [d, d]
+    wqkv: "object"  # [(H + 2 Hkv) Dh, d] = [wq | wk | wv]^T
+    wo: "object"  # [d, d] = wo^T
     mlp_norm: "object"
-    wgu: "object"  # [d, 2 d_ff] (gate | up)
-    wdown: "object"  # [d_ff, d]
+    wgu: "object"  # [2 d_ff, d]: gate^T / up^T rows interleaved in gu_block blocks
+    wdown: "object"  # [d, d_ff] = w_down^T
 
 
 @dataclass
@@ -236,8 +266,12 @@ class DeviceWeights:
     embedding: "object"
     layers: List[DeviceLayer]
     final_norm: "object"
-    out_head: "object"
+    out_head: "object"  # [vocab, d] = out_head^T
     fingerprint_value: int = 0
+
+    @property
+    def gu_block(self) -> int:
+        return gu_block_for(self.config.d_ff)
 
     def fingerprint(self) -> int:
         return self.fingerprint_value
@@ -264,18 +298,19 @@ class DeviceWeights:
         def up(a, dtype=dt):
             return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(device=device, dtype=dtype)
 
+        blk = gu_block_for(weights.config.d_ff)
         layers = []
         for lw in weights.layers:
             layers.append(DeviceLayer(
                 attn_norm=up(lw.attn_norm, torch.float32),
-                wqkv=up(np.concatenate([lw.wq, lw.wk, lw.wv], axis=1)),
-                wo=up(lw.wo),
+                wqkv=up(np.concatenate([lw.wq, lw.wk, lw.wv], axis=1).T),
+                wo=up(np.asarray(lw.wo).T),
                 mlp_norm=up(lw.mlp_norm, torch.float32),
-                wgu=up(np.concatenate([lw.w_gate, lw.w_up], axis=1)),
-                wdown=up(lw.w_down),
+                wgu=up(interleave_gu(np.asarray(lw.w_gate).T, np.asarray(lw.w_up).T, blk)),
+                wdown=up(np.asarray(lw.w_down).T),
             ))
         return cls(weights.config, precision, up(weights.embedding), layers, up(weights.final_norm, torch.float32),
-                   up(weights.out_head), fingerprint_value=weights.fingerprint())
+                   up(np.asarray(weights.out_head).T), fingerprint_value=weights.fingerprint())
 
     @classmethod
     def random(cls, config: ModelConfig, seed: int, precision: str = "bf16", device="cuda") -> "DeviceWeights":
@@ -300,16 +335,16 @@ class DeviceWeights:
         s_in, s_down = 1.0 / np.sqrt(d), 1.0 / np.sqrt(dff)
         emb = draw((config.vocab_size, d), 1.0)
         layers = []
-        for _ in range(config.n_layers):
+        for _ in range(config.n_layers):  # i.i.d. draws: stored directly in the "out x in" layout
             layers.append(DeviceLayer(
                 attn_norm=torch.ones(d, dtype=torch.float32, device=device),
-                wqkv=draw((d, d + 2 * kv), s_in),
+                wqkv=draw((d + 2 * kv, d), s_in),
                 wo=draw((d, d), s_in),
                 mlp_norm=torch.ones(d, dtype=torch.float32, device=device),
-                wgu=draw((d, 2 * dff), s_in),
-                wdown=draw((dff, d), s_down),
+                wgu=draw((2 * dff, d), s_in),
+                wdown=draw((d, dff), s_down),
             ))
-        head = draw((d, config.vocab_size), s_in)
+        head = draw((config.vocab_size, d), s_in)
         h = hashlib.blake2b(repr((config, seed, precision, "device-random")).encode(), digest_size=8)
         return cls(config, precision, emb, layers, torch.ones(d, dtype=torch.float32, device=device), head,
                    fingerprint_value=int.from_bytes(h.digest(), "little"))
@@ -320,11 +355,13 @@ class DeviceWeights:
 
         c = self.config
         hd = lambda t: t.detach().to(torch.float64).cpu().numpy()  # noqa: E731
+        ht = lambda t: np.ascontiguousarray(hd(t).T)  # noqa: E731  ("out x in" -> the reference's [in, out])
         qd, kvd = c.d_model, c.kv_dim
         layers = []
         for dl in self.layers:
-            qkv = hd(dl.wqkv)
-            gu = hd(dl.wgu)
+            qkv = ht(dl.wqkv)
+            g_t, u_t = deinterleave_gu(hd(dl.wgu), self.gu_block)
             layers.append(LayerWeights(hd(dl.attn_norm), qkv[:, :qd], qkv[:, qd:qd + kvd], qkv[:, qd + kvd:],
-                                       hd(dl.wo), hd(dl.mlp_norm), gu[:, :c.d_ff], gu[:, c.d_ff:], hd(dl.wdown)))
-        return Weights(c, hd(self.embedding), layers, hd(self.final_norm), hd(self.out_head))
+                                       ht(dl.wo), hd(dl.mlp_norm), np.ascontiguousarray(g_t.T),
+                                       np.ascontiguousarray(u_t.T), ht(dl.wdown)))
+        return Weights(c, hd(self.embedding), layers, hd(self.final_norm), ht(self.out_head))

@@ -444,8 +444,7 @@ def sharded_recompute(weights, shard: Shard, cache: AssembledCache, selected_glo
             return E.merge_partials(torch.stack(back_ctx), torch.stack(back_ml))
         return merge_query_states(back_ctx, back_ml).to(q_local.dtype)
 
-    E.layer_stack(weights, ids, sel_g, cache.keys, cache.values, dst, sel_g, attn_fn=attn_fn,
-                  fused_residual=not isinstance(comm, ThreadComm))
+    E.layer_stack(weights, ids, sel_g, cache.keys, cache.values, dst, sel_g, attn_fn=attn_fn)
     d = dst.cpu().numpy()
     cache.row_positions[d] = sel_g.cpu().numpy()
     cache.provenance[d] = int(Provenance.RECOMPUTED_GLOBAL)

@@ -37,3 +37,10 @@ def cuda():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return torch.device("cuda")
+
+
+@pytest.fixture(scope="session")
+def T(cuda):
+    import torch
+
+    return torch

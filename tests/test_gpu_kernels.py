@@ -11,13 +11,6 @@ import oracle as O
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def T(cuda):
-    import torch
-
-    return torch
-
-
 def test_rope_table_fp64_angles(T, cuda):
     from paper_2603_05353_b200 import engine as E
 
@@ -269,8 +262,8 @@ def test_stream_handle_follows_torch_current_stream(T, cuda):
 @pytest.mark.parametrize("P,R,K,N", [(3, 32, 4096, 6144), (3, 32, 14336, 4096), (1, 32, 512, 1536),
                                      (3, 64, 512, 3584), (2, 96, 1024, 256)])
 def test_prompt_mm_weight_stream_gemm(T, cuda, P, R, K, N):
-    """ifkv_prompt_mm (tcgen05, MN-major weight operand, K splits) against
-    an fp64 product of the same bf16 operands: fp32 accumulation only."""
+    """ifkv_prompt_mm (tcgen05, K-major "out x in" weight operand, K splits)
+    against an fp64 product of the same bf16 operands: fp32 accumulation only."""
     from paper_2603_05353_b200 import _native as NV
     from paper_2603_05353_b200 import engine as E
 
@@ -286,11 +279,12 @@ def test_prompt_mm_weight_stream_gemm(T, cuda, P, R, K, N):
     # for the same bf16 operands (~1e-5 at K = 14336)
     cub = rel(sum(T.mm(x[p], w, out_dtype=T.float32).double() for p in range(P)))
     tol = max(1e-5, 2 * cub)
+    wt = w.t().contiguous()  # the device layout: [N][K]
     for s in sorted({1, E.prompt_mm_splits(N, K, R, 148, P), min(K // 64, 7)}):
         out = T.full((s, R, N), float("nan"), dtype=T.float32, device="cuda")
-        NV.call("ifkv_prompt_mm", NV.ptr(x), P, R, K, NV.ptr(w), N, s, NV.ptr(out), NV.stream_handle())
+        NV.call("ifkv_prompt_mm", NV.ptr(x), P, R, K, NV.ptr(wt), N, s, NV.ptr(out), NV.stream_handle())
         assert rel(out.double().sum(0)) < tol, (s, cub)
-    assert rel(E.mm_parts(x, w).double().sum(0)) < tol
+    assert rel(E.mm_parts(x, wt).double().sum(0)) < tol
     from paper_2603_05353_b200.errors import ConfigurationError
 
     with pytest.raises(ConfigurationError):
