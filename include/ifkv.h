@@ -169,11 +169,14 @@ int ifkv_prompt_attn_partial(int kv_dtype, const float* qd, const void* k_slab, 
                              float* part_ml, float* part_o, void* stream);
 /* Merge the partials of each group's items in a fixed order -- its context
  * items [item_begin[g], item_begin[g+1]) then, if prompt_item0 >= 0, its
- * prompt item prompt_item0 + g: ctx [G][M][H][Dh] fp32, final ml [G][H][M][2];
- * ctx_split3 (optional, bf16 [3][G*M][H*Dh]) also receives its hi/mid/lo terms
- * (the O-projection GEMM operand). */
+ * prompt items prompt_item0 + g * n_prompt_items + [0, n_prompt_items) (the
+ * prompt's own keys in blocks of <= 128, so any prompt length M works):
+ * ctx [G][M][H][Dh] fp32, final ml [G][H][M][2]; ctx_split3 (optional, bf16
+ * [3][G*M][H*Dh]) also receives its hi/mid/lo terms (the O-projection GEMM
+ * operand). */
 int ifkv_prompt_attn_merge(const float* part_ml, const float* part_o, const int32_t* item_begin, int prompt_item0,
-                           int G, int H, int M, int Dh, float* ctx, float* ml, void* ctx_split3, void* stream);
+                           int n_prompt_items, int G, int H, int M, int Dh, float* ctx, float* ml, void* ctx_split3,
+                           void* stream);
 /* Capture-layer column scores (score_from_attention selection.py:108-124):
  * for each scored item column j, scores[key_row0 + j] =
  * (1/H) sum_h sum_m exp(s_hmj - m_hm) / l_hm, deterministic order. */

@@ -123,24 +123,25 @@ __global__ void __launch_bounds__(256) prompt_attn_partial_kernel(
 
 // grid (G * H * M), 256 threads = 8 warps: merge the group's items.
 // Items of group g: [item_begin[g], item_begin[g+1]) then, if
-// prompt_item0 >= 0, item prompt_item0 + g (the group's causal prompt item).
+// prompt_item0 >= 0, items prompt_item0 + g * n_prompt + [0, n_prompt) (the
+// group's causal prompt items: its prompt keys in blocks of <= 128).
 // Warp w takes items k = w, w + 8, ...; lane owns Dh/32 (<= 4) consecutive
 // dims as one vector load.  Warp partials combine in warp order through smem
 // (fixed order -> deterministic).
 __global__ void __launch_bounds__(256) prompt_attn_merge_kernel(
     const float* __restrict__ part_ml, const float* __restrict__ part_o, const int32_t* __restrict__ item_begin,
-    int prompt_item0, int H, int M, int Dh, float* __restrict__ ctx, float* __restrict__ ml,
+    int prompt_item0, int n_prompt, int H, int M, int Dh, float* __restrict__ ctx, float* __restrict__ ml,
     __nv_bfloat16* __restrict__ ctx3, int64_t plane) {
   __shared__ float s_m[8], s_l[8];
   __shared__ float s_o[8][256];
   const int r = blockIdx.x;  // (g, h, m)
   const int m = r % M, h = (r / M) % H, g = r / (M * H);
   const int b = item_begin[g], e = item_begin[g + 1];
-  const int n = e - b + (prompt_item0 >= 0 ? 1 : 0);
+  const int n = e - b + (prompt_item0 >= 0 ? n_prompt : 0);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int per = (Dh + 31) / 32;  // dims per lane (<= 8)
   auto row_of = [&](int k) -> int64_t {
-    const int it = k < e - b ? b + k : prompt_item0 + g;
+    const int it = k < e - b ? b + k : prompt_item0 + g * n_prompt + (k - (e - b));
     return ((int64_t)it * H + h) * M + m;
   };
   // pass 1: max over all items (every warp computes it redundantly -> no sync)
@@ -266,11 +267,12 @@ extern "C" int ifkv_prompt_attn_partial(int kv_dtype, const float* qd, const voi
 }
 
 extern "C" int ifkv_prompt_attn_merge(const float* part_ml, const float* part_o, const int32_t* item_begin,
-                                      int prompt_item0, int G, int H, int M, int Dh, float* ctx, float* ml,
-                                      void* ctx_split3, void* stream) {
+                                      int prompt_item0, int n_prompt_items, int G, int H, int M, int Dh, float* ctx,
+                                      float* ml, void* ctx_split3, void* stream) {
   IFKV_CHECK_ARG(Dh <= 256 && G > 0, "prompt_attn_merge: bad shape");
+  IFKV_CHECK_ARG(prompt_item0 < 0 || n_prompt_items >= 1, "prompt_attn_merge: n_prompt_items must be >= 1");
   prompt_attn_merge_kernel<<<G * H * M, 256, 0, as_stream(stream)>>>(
-      part_ml, part_o, item_begin, prompt_item0, H, M, Dh, ctx, ml, (__nv_bfloat16*)ctx_split3,
+      part_ml, part_o, item_begin, prompt_item0, n_prompt_items, H, M, Dh, ctx, ml, (__nv_bfloat16*)ctx_split3,
       (int64_t)G * M * H * Dh);
   IFKV_LAUNCH_CHECK("prompt_attn_merge");
   return IFKV_OK;

@@ -104,40 +104,18 @@ __global__ void __launch_bounds__(128) recompute_attn_simt_kernel(const T* __res
 
 using namespace ifkv;
 
-extern "C" int ifkv_recompute_attn_tc(const void* q, const void* k_layer, const void* v_layer, const int64_t* horizon,
-                                      int S, int H, int Hkv, int Dh, int n_rows, float scale, void* out, float* ml_out,
-                                      void* stream);
-
-extern "C" int ifkv_recompute_attn_tc_v4(const void* q, const void* k_layer, const void* v_layer,
-                                         const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows,
-                                         float scale, void* out, float* ml_out, void* stream);
 extern "C" int ifkv_recompute_attn_tc_v5(const void* q, const void* k_layer, const void* v_layer,
                                          const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows,
                                          float scale, void* out, float* ml_out, void* stream);
-// tcgen05 kernel generation: v5 for every grid (two ping-ponging tiles per
+// The tcgen05 kernel (tc_recompute_attn_v5.cu): two ping-ponging tiles per
 // CTA, P staged in smem so S(j+1) follows the read of S(j); tiles of
-// floor(128/G) tokens x G heads; key splits below two waves).  Measured
-// against v4 (one tile per CTA, triple-buffered S, column-split softmax):
-// G = 4, ms per layer at the C2 shape: k = 1639 0.445-0.48 vs 0.47-0.52,
-// k = 2458 0.57-0.64 vs 0.64-0.74, k = 3277 0.79-0.94 vs 0.84-0.98, k = 4916
-// 1.07-1.20 vs 1.23-1.42; G = 7: k = 1639 0.38-0.40 vs 0.41-0.43, k = 4916
-// 0.94-1.05 vs 1.07-1.26 (profiles/r1_attn_ab.md).  IFKV_ATTN_GEN=2/4/5 pins
-// one generation (A/B).
-#ifndef IFKV_ATTN_GEN
-#define IFKV_ATTN_GEN 0
-#endif
+// floor(128/G) tokens x G heads; key splits below two waves.  Earlier
+// generations (v2: P in TMEM; v4: one tile per CTA, triple-buffered S) were
+// measured slower at every C2/C4 grid (profiles/r1_attn_ab.md) and removed.
 static int recompute_attn_tc_any(const void* q, const void* k_layer, const void* v_layer, const int64_t* horizon,
                                  int S, int H, int Hkv, int Dh, int n_rows, float scale, void* out, float* ml_out,
                                  void* stream) {
-  int gen = IFKV_ATTN_GEN;
-  if (gen == 0) gen = 5;
-  if (gen == 5)
-    return ifkv_recompute_attn_tc_v5(q, k_layer, v_layer, horizon, S, H, Hkv, Dh, n_rows, scale, out, ml_out,
-                                     stream);
-  if (gen == 4)
-    return ifkv_recompute_attn_tc_v4(q, k_layer, v_layer, horizon, S, H, Hkv, Dh, n_rows, scale, out, ml_out,
-                                     stream);
-  return ifkv_recompute_attn_tc(q, k_layer, v_layer, horizon, S, H, Hkv, Dh, n_rows, scale, out, ml_out, stream);
+  return ifkv_recompute_attn_tc_v5(q, k_layer, v_layer, horizon, S, H, Hkv, Dh, n_rows, scale, out, ml_out, stream);
 }
 
 static int recompute_attn_simt_impl(int dtype, const void* q, const void* k_layer, const void* v_layer,

@@ -30,6 +30,7 @@ from . import _native as N
 from .errors import ConfigurationError
 
 ITEM_KEYS = 128  # keys per prompt-attention work item (<= kItemKeysMax)
+PROMPT_ITEM_KEYS = 128  # prompt keys per causal prompt item
 
 # Optional CUDA-event brackets around named kernels: {name: [(start, end, work)]}
 # (the benchmark sets this to measure per-launch durations for the roofline).
@@ -405,8 +406,9 @@ def segments_from_deltas(deltas: np.ndarray, row_offset: int = 0) -> List[Tuple[
 
 def _plan_items(groups: Sequence[PromptGroup], M: int, item_keys: int = ITEM_KEYS):
     """Work items (24-byte ifkv_attn_item rows): every group's context items
-    (<= ITEM_KEYS keys of one constant-delta run), groups in order, then one
-    causal prompt item per group.  Returns (items, ctx_begin [G+1], n_ctx,
+    (<= ITEM_KEYS keys of one constant-delta run), groups in order, then each
+    group's causal prompt items (its M prompt keys in blocks of <= 128, so
+    any prompt length works).  Returns (items, ctx_begin [G+1], n_ctx,
     qset_group, qset_cs, deltas)."""
     deltas = sorted({d for g in groups for (_, _, d) in g.segments if d != 0})
     delta_id = {d: i for i, d in enumerate(deltas)}
@@ -429,7 +431,8 @@ def _plan_items(groups: Sequence[PromptGroup], M: int, item_keys: int = ITEM_KEY
         ctx_begin.append(len(items))
     n_ctx = len(items)
     for gi in range(len(groups)):
-        items.append((gi, qset(gi, 0), 0, M, 1, 0))
+        for k0 in range(0, M, PROMPT_ITEM_KEYS):
+            items.append((gi, qset(gi, 0), k0, min(PROMPT_ITEM_KEYS, M - k0), 1, 0))
     return (np.asarray(items, dtype=np.int32).reshape(-1, 6), np.asarray(ctx_begin, np.int32), n_ctx,
             np.asarray(qset_group, np.int32), np.asarray(qset_cs, np.int32), deltas)
 
@@ -526,10 +529,11 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
                        _s())
             if include_prompt:
                 N.call("ifkv_prompt_attn_partial", kv_dt, N.ptr(qd), N.ptr(slab_k[li]), N.ptr(slab_v[li]), N.ptr(kp),
-                       N.ptr(vp), prompt_items_p, n_items - n_ctx, M, H, Hkv, M, Dh, scale,
+                       N.ptr(vp), prompt_items_p, n_items - n_ctx, min(M, PROMPT_ITEM_KEYS), H, Hkv, M, Dh, scale,
                        part_ml.data_ptr() + n_ctx * stride_ml, part_o.data_ptr() + n_ctx * stride_o, _s())
             fuse_split = bf16 and merge_hook is None and not capture
-            N.call("ifkv_prompt_attn_merge", N.ptr(part_ml), N.ptr(part_o), ib_p, n_ctx if include_prompt else -1, G,
+            N.call("ifkv_prompt_attn_merge", N.ptr(part_ml), N.ptr(part_o), ib_p, n_ctx if include_prompt else -1,
+                   -(-M // PROMPT_ITEM_KEYS), G,
                    H, M, Dh, N.ptr(ctx), N.ptr(ml), N.ptr(ctx3) if fuse_split else None, _s())
             if merge_hook is not None:
                 ctx_m, ml_m = merge_hook(ctx, ml)

@@ -73,11 +73,26 @@ class RecomputePlan:
 
 def make_plan(cache: AssembledCache, selected) -> RecomputePlan:
     """Standard plan: positions = horizons = the selected indices
-    (recompute.py:56-64).  A device tensor from select_topk is already
-    sorted, unique and in range and is used as is (no host sync)."""
+    (recompute.py:56-64).  A device tensor produced by select_topk (tagged:
+    sorted, unique, in range by construction) is used as is with no host
+    sync; any other device tensor is sorted and validated on the device with
+    one deferred host check (range, duplicates), like the reference's host
+    checks."""
     torch = _torch()
     if isinstance(selected, torch.Tensor) and selected.is_cuda:
-        sel = selected.to(torch.int64)
+        n = cache.context_length
+        tag = getattr(selected, "_ifkv_valid_plan", None)
+        if tag is not None and tag <= n:
+            sel = selected.to(torch.int64)
+            return RecomputePlan(selected=sel, positions=sel, allowed_upto=sel, trusted=True)
+        sel = torch.sort(selected.reshape(-1).to(torch.int64)).values
+        if sel.numel():
+            bad = (sel[0] < 0) | (sel[-1] >= n)
+            dup = bool((sel[1:] == sel[:-1]).any().item()) if sel.numel() > 1 else False
+            if bool(bad.item()):
+                raise ConfigurationError(f"selected index outside context [0, {n})")
+            if dup:
+                raise ConfigurationError("selected indices contain duplicates")
         return RecomputePlan(selected=sel, positions=sel, allowed_upto=sel, trusted=True)
     sel = np.sort(np.asarray(selected, dtype=np.int64).ravel())
     n = cache.context_length

@@ -148,19 +148,30 @@ def score_attention_norm(weights, cache: AssembledCache, prompt_token_ids, posit
 
 def select_topk(scores, k: int):
     """Indices of the k largest scores, ties to the lower index, ascending
-    (selection.py:172-183).  Device int64 tensor."""
+    (selection.py:172-183).  Device int64 tensor, tagged as a valid recompute
+    plan (sorted, unique, in range) for ``make_plan``.
+
+    fp32 scores (attention-norm) run the exact radix select
+    (``ifkv_topk_segments``); fp64 scores (the CacheBlend baseline, summed in
+    fp64) keep their precision: a stable descending sort on the device, so
+    near-equal fp64 scores are not collapsed into fp32 ties."""
     torch = _torch()
     if not isinstance(scores, torch.Tensor):
-        scores = torch.as_tensor(np.asarray(scores), dtype=torch.float32, device="cuda")
-    scores = scores.to(torch.float32).contiguous()
+        a = np.asarray(scores)
+        scores = torch.as_tensor(a, dtype=torch.float64 if a.dtype == np.float64 else torch.float32, device="cuda")
     n = scores.numel()
     if k > n:
         raise ConfigurationError(f"k ({k}) exceeds score count ({n})")
     if k < 0:
         raise ConfigurationError(f"k must be >= 0, got {k}")
     if k == 0:
-        return torch.zeros(0, dtype=torch.int64, device=scores.device)
-    idx, _, _ = E.topk_segments(scores, [0, n], [k])
+        idx = torch.zeros(0, dtype=torch.int64, device=scores.device)
+    elif scores.dtype == torch.float64:
+        order = torch.sort(scores.contiguous(), descending=True, stable=True).indices[:k]
+        idx = torch.sort(order).values
+    else:
+        idx, _, _ = E.topk_segments(scores.to(torch.float32).contiguous(), [0, n], [k])
+    idx._ifkv_valid_plan = n  # produced here: sorted, unique, in [0, n)
     return idx
 
 

@@ -314,6 +314,16 @@ def sharded_select(weights, shard: Shard, cache: AssembledCache, prompt_token_id
     for its local rows."""
     torch = _torch()
     cfg = weights.config
+    from .positions import GeometryConfig, GeometryMode
+    from .selection import Strategy
+
+    if config.strategy != Strategy.ATTENTION_NORM:
+        raise ConfigurationError(f"sharded selection implements the attention-norm strategy only, got "
+                                 f"{config.strategy.value!r}")
+    geo = config.geometry
+    mode = geo.mode if isinstance(geo, GeometryConfig) else (GeometryMode.parse(geo) if geo is not None else None)
+    if mode not in (None, GeometryMode.GLOBAL):
+        raise ConfigurationError(f"sharded selection scores under GLOBAL geometry only, got {mode.value!r}")
     prompt = np.asarray(prompt_token_ids, np.int64)
     n_local = cache.context_length
     if n_local != shard.global_rows.size:

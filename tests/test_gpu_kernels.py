@@ -196,10 +196,10 @@ def test_recompute_attention_unsorted_and_empty_horizons(T, cuda, partial, n_emp
 
 
 @pytest.mark.parametrize("partial", [False, True])
-def test_recompute_attention_large_grid_v2_path(T, cuda, partial):
-    """A grid of >= two waves (k = 2600 at 32 q / 8 kv heads) runs the two-tile
-    ping-pong kernel (small grids run v4): compare with the SIMT kernel on every
-    row and with the oracle on sampled rows."""
+def test_recompute_attention_large_grid_tcgen05(T, cuda, partial):
+    """k = 2600 at 32 q / 8 kv heads (a grid near two waves, so the key-split
+    path of the tcgen05 kernel is exercised): compare with the SIMT kernel on
+    every row and with the oracle on sampled rows."""
     from paper_2603_05353_b200 import engine as E
 
     rng = np.random.default_rng(5)
@@ -232,8 +232,9 @@ def test_recompute_attention_large_grid_v2_path(T, cuda, partial):
 
 @pytest.mark.parametrize("H,hkv,k", [(28, 4, 300), (28, 4, 2600), (24, 8, 2600)])
 def test_recompute_attention_gqa_groups_not_dividing_128(T, cuda, H, hkv, k):
-    """G = 7 (Qwen2.5-VL: 18 tokens x 7 heads = 126 rows per tile, v4 path) and
-    G = 3 (42 tokens x 3 heads) against the oracle on sampled rows."""
+    """G = 7 (Qwen2.5-VL: 18 tokens x 7 heads = 126 rows per tile) and G = 3
+    (42 tokens x 3 heads) on the tcgen05 kernel against the oracle on sampled
+    rows."""
     from paper_2603_05353_b200 import engine as E
 
     rng = np.random.default_rng(H + k)

@@ -93,6 +93,23 @@ def test_c1_reorder_bit_exact(c1):
     assert rel_err(second.scores_numpy(), scores) <= 1e-4
 
 
+def test_long_prompt_over_128_tokens_matches_oracle(cuda):
+    """A 200-token prompt (the causal prompt keys span two 128-key items):
+    selection bit-exact against the oracle."""
+    P = _pkg()
+    task = P.SyntheticTask(kind="uniform_noise", total_length=1024, fixed_size=256, prompt_length=32,
+                           vocab_size=1024)
+    dw, ow, g = _setup(P.c1_config(), 7, "bf16", task, 3)
+    prompt = np.random.default_rng(3).integers(0, 1024, size=200)  # (the task generator caps prompts at its band)
+    kvs = [P.prefill_chunk(dw, c) for c in g.chunks]
+    cache = P.assemble(kvs)
+    res = P.run_selection(dw, g.chunks, cache, prompt, P.SelectionConfig(ratio=0.15))
+    oc = O.assemble([oracle_chunk(c) for c in kvs])
+    scores, sel = O.run_selection(ow, oc, prompt, ratio=0.15)
+    np.testing.assert_allclose(res.scores_numpy(), scores, rtol=1e-4, atol=0)
+    np.testing.assert_array_equal(res.selected_numpy(), sel)
+
+
 # ---------------------------------------------------------------------------
 # fp32 mode: the reference's tiny configs, 1e-4 bars
 # ---------------------------------------------------------------------------

@@ -100,6 +100,11 @@ def test_segments_and_work_items():
     assert items[:, 4].tolist() == [0, 0, 0, 0, 0, 1, 1]
     assert items[:, 0].tolist() == [0, 0, 0, 0, 1, 0, 1]
     assert qg.tolist() == [0, 0, 1, 1] and qc.tolist() == [0, -1, 0, -1]
+    # prompts longer than 128 tokens: the causal prompt keys split into <= 128-key items
+    long = [E.PromptGroup(np.arange(300), np.arange(300), [(0, 10, 0)])]
+    items, begin, n_ctx, _, _, _ = E._plan_items(long, 300)
+    assert n_ctx == 1 and items[1:, 2].tolist() == [0, 128, 256] and items[1:, 3].tolist() == [128, 128, 44]
+    assert items[1:, 4].tolist() == [1, 1, 1]
 
 
 def test_score_from_attention_seam():

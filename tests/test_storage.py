@@ -31,10 +31,17 @@ def test_bf16_round_trip(tmp_path, golden_small):
     src = tmp_path / "a.ifkc"
     src.write_bytes(golden_small["tiny_ifkc_f64"].tobytes())
     ckv = load_cache(src, device="cpu", dtype=torch.bfloat16)
-    save_cache(ckv, tmp_path / "b.ifkc")
+    save_cache(ckv, tmp_path / "b.ifkc", precision="bf16")  # the compact native file (code 2)
     back = load_cache(tmp_path / "b.ifkc", device="cpu")
     assert back.keys.dtype == torch.bfloat16
     assert torch.equal(back.keys, ckv.keys) and torch.equal(back.values, ckv.values)
+    # default: a bf16 cache is written as exact f32 (code 0), which the reference can read
+    save_cache(ckv, tmp_path / "c.ifkc")
+    raw = (tmp_path / "c.ifkc").read_bytes()
+    n_id = int.from_bytes(raw[16:20], "little")
+    assert raw[20 + n_id + 16 + 1] == 0  # precision code byte
+    f32 = load_cache(tmp_path / "c.ifkc", device="cpu")
+    assert f32.keys.dtype == torch.float32 and torch.equal(f32.keys, ckv.keys.float())
 
 
 @pytest.mark.parametrize("how", ["flip", "version", "magic", "truncate"])
@@ -52,3 +59,30 @@ def test_corruption_detected(tmp_path, golden_small, how):
     p.write_bytes(bytes(data))
     with pytest.raises(DataFormatError):
         load_cache(p, device="cpu")
+
+
+@pytest.mark.gpu
+def test_reference_files_load_into_hbm(golden_small, tmp_path, cuda):
+    """IFKC files the reference wrote (f64 and f32) straight into HBM, as
+    stored and converted on the device (f32, bf16), via one pinned read."""
+    paths = []
+    for key in ("tiny_ifkc_f64", "tiny_ifkc_f32"):
+        paths.append(tmp_path / f"{key}.ifkc")
+        paths[-1].write_bytes(golden_small[key].tobytes())
+    f64 = load_cache(paths[0], device="cuda")
+    assert f64.keys.is_cuda and f64.keys.dtype == torch.float64
+    np.testing.assert_array_equal(f64.keys.cpu().numpy(), golden_small["tiny_chunk_keys"][1])
+    np.testing.assert_array_equal(f64.values.cpu().numpy(), golden_small["tiny_chunk_values"][1])
+    as32 = load_cache(paths[0], device="cuda", dtype=torch.float32)
+    np.testing.assert_array_equal(as32.keys.cpu().numpy(), golden_small["tiny_chunk_keys"][1].astype(np.float32))
+    as16 = load_cache(paths[0], device="cuda", dtype=torch.bfloat16)
+    assert torch.equal(as16.keys, f64.keys.to(torch.bfloat16))
+    from paper_2603_05353_b200.storage import load_caches
+
+    both = load_caches(paths, device="cuda", dtype=torch.float32)
+    np.testing.assert_array_equal(both[1].keys.cpu().numpy(), golden_small["tiny_ifkc_f32_keys"])
+    assert both[0].chunk_id == "c1" and both[0].length == 8
+    # a device bf16 cache written by default as f32 reloads bit-identically
+    save_cache(as16, tmp_path / "back.ifkc")
+    back = load_cache(tmp_path / "back.ifkc", device="cuda", dtype=torch.bfloat16)
+    assert torch.equal(back.keys, as16.keys) and torch.equal(back.values, as16.values)
