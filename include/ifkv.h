@@ -182,6 +182,16 @@ int ifkv_prompt_attn_merge(const float* part_ml, const float* part_o, const int3
  * (1/H) sum_h sum_m exp(s_hmj - m_hm) / l_hm, deterministic order. */
 int ifkv_score_columns(int kv_dtype, const float* qd, const void* k_slab, const ifkv_attn_item* items, int n_items,
                        const float* ml, int H, int Hkv, int M, int Dh, float scale, float* scores, void* stream);
+/* Prompt-row q/k/v of the scoring pass in one pass (model.py:435-437 for the
+ * prompt rows + the query-side form of the key re-rotation,
+ * selection.py:152-158): qkv = sum of n_parts fp32 blocks [G*M][(H+2Hkv)Dh];
+ * q, k rotated by cs[row]; kp, vp fp32 [G*M][Hkv][Dh]; for every query set s
+ * of the row's group g (qs_list[qs_begin[g] .. qs_begin[g+1])) qd[s][h][m] =
+ * R(-cs_delta[qset_cs[s]]) q (qset_cs < 0: no rotation), qd3 (optional) its
+ * bf16 hi/mid/lo terms [n_qsets][3][H][M][Dh]. */
+int ifkv_prompt_qkv(const float* qkv, int n_parts, int G, int M, int H, int Hkv, int Dh, const float* cs,
+                    const int32_t* qs_begin, const int32_t* qs_list, const int32_t* qset_cs, const float* cs_delta,
+                    float* kp, float* vp, float* qd, void* qd3, void* stream);
 /* Rotated query sets: qd[s] = R(-cs[qset_cs[s]]) q[qset_group[s]], transposed
  * from q [G][M][H][Dh] to [H][M][Dh]; qset_cs[s] < 0 means no rotation.
  * qd3 (optional, bf16 [n_qsets][3][H][M][Dh]) receives the hi/mid/lo split

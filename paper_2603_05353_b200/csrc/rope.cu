@@ -290,6 +290,70 @@ __global__ void rotate_queries_kernel(const float* __restrict__ q, int M, int H,
   }
 }
 
+// Prompt-row q/k/v of the scoring pass in one pass (replaces
+// qkv_rope_scatter + rotate_queries there): the n_parts fp32 GEMM partials
+// summed in a fixed order, q and k rotated to the prompt positions (cs), k/v
+// written compact fp32 [rows][Hkv][Dh], and q rotated once more by -delta for
+// each of its group's query sets (q . R(d) k == (R(-d) q) . k, the context
+// keys stay as stored) into qd [s][H][M][Dh] (+ the bf16 split terms qd3).
+// Group g's query sets: qs_list[qs_begin[g] .. qs_begin[g+1]).
+__global__ void prompt_qkv_kernel(const float* __restrict__ qkv, int n_parts, int64_t part_stride, int G, int M,
+                                  int H, int Hkv, int Dh, const float2* __restrict__ cs,
+                                  const int32_t* __restrict__ qs_begin, const int32_t* __restrict__ qs_list,
+                                  const int32_t* __restrict__ qset_cs, const float2* __restrict__ cs_delta,
+                                  float* __restrict__ kp, float* __restrict__ vp, float* __restrict__ qd,
+                                  __nv_bfloat16* __restrict__ qd3) {
+  const int half = Dh / 2;
+  const int width_pairs = (H + 2 * Hkv) * half;
+  const int rows = G * M;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)rows * width_pairs) return;
+  const int r = (int)(t / width_pairs), c = (int)(t % width_pairs);
+  const float* src = qkv + (int64_t)r * (H + 2 * Hkv) * Dh + 2 * c;
+  float x0 = 0.f, x1 = 0.f;
+  for (int p = 0; p < n_parts; ++p) {
+    x0 += src[p * part_stride];
+    x1 += src[p * part_stride + 1];
+  }
+  const int head = c / half, pi = c % half;
+  if (head < H + Hkv) {
+    const float2 a = cs[(int64_t)r * half + pi];
+    const float y0 = x0 * a.x - x1 * a.y, y1 = x0 * a.y + x1 * a.x;
+    x0 = y0;
+    x1 = y1;
+  }
+  if (head >= H) {
+    float* d = (head < H + Hkv ? kp + ((int64_t)r * Hkv + (head - H)) * Dh
+                               : vp + ((int64_t)r * Hkv + (head - H - Hkv)) * Dh) + 2 * pi;
+    d[0] = x0;
+    d[1] = x1;
+    return;
+  }
+  const int g = r / M, m = r % M;
+  const int64_t plane = (int64_t)H * M * Dh;
+  for (int k = qs_begin[g]; k < qs_begin[g + 1]; ++k) {
+    const int s = qs_list[k], ci = qset_cs[s];
+    float y0 = x0, y1 = x1;
+    if (ci >= 0) {
+      const float2 a = cs_delta[(int64_t)ci * half + pi];
+      y0 = x0 * a.x + x1 * a.y;  // rotation by -angle
+      y1 = -x0 * a.y + x1 * a.x;
+    }
+    const int64_t o = (((int64_t)s * H + head) * M + m) * Dh + 2 * pi;
+    qd[o] = y0;
+    qd[o + 1] = y1;
+    if (qd3) {  // [n_qsets][3][H][M][Dh]
+      const int64_t o3 = ((int64_t)s * 3) * plane + (o - (int64_t)s * plane);
+      __nv_bfloat16 a0, a1, a2, b0, b1, b2;
+      split3(y0, a0, a1, a2);
+      split3(y1, b0, b1, b2);
+      reinterpret_cast<__nv_bfloat162*>(qd3 + o3)[0] = __halves2bfloat162(a0, b0);
+      reinterpret_cast<__nv_bfloat162*>(qd3 + o3 + plane)[0] = __halves2bfloat162(a1, b1);
+      reinterpret_cast<__nv_bfloat162*>(qd3 + o3 + 2 * plane)[0] = __halves2bfloat162(a2, b2);
+    }
+  }
+}
+
 // Fresh q/k/v epilogue: rope q and k at the rows' positions, write q
 // compact, scatter k and v into the destination rows.
 template <typename TIn, typename TOut>
@@ -608,6 +672,20 @@ extern "C" int ifkv_rotate_queries(const float* q, int G, int M, int H, int Dh, 
       q, M, H, Dh, qset_group, qset_cs, n_qsets, reinterpret_cast<const float2*>(cs), qd,
       reinterpret_cast<__nv_bfloat16*>(qd3));
   IFKV_LAUNCH_CHECK("rotate_queries");
+  return IFKV_OK;
+}
+
+extern "C" int ifkv_prompt_qkv(const float* qkv, int n_parts, int G, int M, int H, int Hkv, int Dh, const float* cs,
+                               const int32_t* qs_begin, const int32_t* qs_list, const int32_t* qset_cs,
+                               const float* cs_delta, float* kp, float* vp, float* qd, void* qd3, void* stream) {
+  IFKV_CHECK_ARG(Dh % 2 == 0 && Hkv > 0 && H > 0 && H % Hkv == 0 && n_parts >= 1 && G > 0 && M > 0,
+                 "prompt_qkv: bad shape");
+  const int64_t total = (int64_t)G * M * (H + 2 * Hkv) * (Dh / 2);
+  const int64_t part_stride = (int64_t)G * M * (H + 2 * Hkv) * Dh;
+  prompt_qkv_kernel<<<(unsigned)((total + 255) / 256), 256, 0, as_stream(stream)>>>(
+      qkv, n_parts, part_stride, G, M, H, Hkv, Dh, reinterpret_cast<const float2*>(cs), qs_begin, qs_list, qset_cs,
+      reinterpret_cast<const float2*>(cs_delta), kp, vp, qd, reinterpret_cast<__nv_bfloat16*>(qd3));
+  IFKV_LAUNCH_CHECK("prompt_qkv");
   return IFKV_OK;
 }
 

@@ -276,6 +276,19 @@ PROMPT_MM = os.environ.get("IFKV_PROMPT_MM", "1") != "0"
 _SMS: List[int] = []
 
 
+_SIDE: dict = {}
+
+
+def _side_stream():
+    """A second stream per device for work that can overlap the current
+    stream's kernels (fork/join through events)."""
+    torch = _torch()
+    dev = torch.cuda.current_device()
+    if dev not in _SIDE:
+        _SIDE[dev] = torch.cuda.Stream(device=dev)
+    return _SIDE[dev]
+
+
 def _sm_count() -> int:
     if not _SMS:
         torch = _torch()
@@ -479,12 +492,16 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
     item_keys = _tc_item_keys(groups, Hkv, H // Hkv, M) if use_tc else ITEM_KEYS
     items_np, ctx_begin_np, n_ctx, qg_np, qc_np, deltas = _plan_items(groups, M, item_keys)
     n_items, n_qsets = items_np.shape[0], qg_np.size
-    meta = h2d(np.concatenate([items_np.ravel(), ctx_begin_np, qg_np, qc_np]), dev)
+    qs_list = np.argsort(qg_np, kind="stable").astype(np.int32)  # each group's query sets, contiguous
+    qs_begin = np.searchsorted(qg_np[qs_list], np.arange(G + 1)).astype(np.int32)
+    meta = h2d(np.concatenate([items_np.ravel(), ctx_begin_np, qg_np, qc_np, qs_begin, qs_list]), dev)
     items_p = meta.data_ptr()
     prompt_items_p = items_p + 24 * n_ctx
     ib_p = items_p + 4 * items_np.size
     qg_p = ib_p + 4 * ctx_begin_np.size
     qc_p = qg_p + 4 * qg_np.size
+    qsb_p = qc_p + 4 * qc_np.size
+    qsl_p = qsb_p + 4 * qs_begin.size
     cs_delta = rope_table(np.asarray(deltas, np.int64) if deltas else np.zeros(1, np.int64), Dh, cfg.rope_base, dev)
     ids = h2d(np.concatenate([np.asarray(g.token_ids, np.int64) for g in groups]), dev)
     pos_all = np.concatenate([np.asarray(g.positions, np.int64) for g in groups])
@@ -496,7 +513,6 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
     rows = G * M
     n_rows = slab_k.shape[1]
     h = embed_rows(weights.embedding, ids)
-    q = torch.empty((rows, H, Dh), dtype=torch.float32, device=dev)
     kp = torch.empty((rows, Hkv, Dh), dtype=torch.float32, device=dev)
     vp = torch.empty_like(kp)
     qd = torch.empty((n_qsets, H, M, Dh), dtype=torch.float32, device=dev)
@@ -515,11 +531,23 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
         lw = weights.layers[li]
         x = add_rmsnorm(h, pending, pending_parts, lw.attn_norm, mode)
         qkv = mm_parts(x, lw.wqkv)
-        qkv_rope_scatter(qkv, qkv.shape[0], H, Hkv, Dh, cs_prompt, q, kp, vp, None)
-        N.call("ifkv_rotate_queries", N.ptr(q), G, M, H, Dh, qg_p, qc_p, n_qsets, N.ptr(cs_delta), N.ptr(qd),
-               N.ptr(qd3), _s())
+        N.call("ifkv_prompt_qkv", N.ptr(qkv), qkv.shape[0], G, M, H, Hkv, Dh, N.ptr(cs_prompt), qsb_p, qsl_p, qc_p,
+               N.ptr(cs_delta), N.ptr(kp), N.ptr(vp), N.ptr(qd), N.ptr(qd3), _s())
         capture = capture_layer is not None and li == capture_layer
         with _Bracket("prompt_attn", li):
+            side = include_prompt and use_tc and n_ctx and torch.cuda.is_available()
+            if side:  # the prompt's own keys (SIMT) on the SMs the tensor-core grid leaves idle
+                fork = torch.cuda.Event()
+                fork.record()
+                side_stream = _side_stream()
+                side_stream.wait_event(fork)
+                with torch.cuda.stream(side_stream):
+                    N.call("ifkv_prompt_attn_partial", kv_dt, N.ptr(qd), N.ptr(slab_k[li]), N.ptr(slab_v[li]),
+                           N.ptr(kp), N.ptr(vp), prompt_items_p, n_items - n_ctx, min(M, PROMPT_ITEM_KEYS), H, Hkv,
+                           M, Dh, scale, part_ml.data_ptr() + n_ctx * stride_ml,
+                           part_o.data_ptr() + n_ctx * stride_o, _s())
+                    join = torch.cuda.Event()
+                    join.record()
             if use_tc and n_ctx:
                 N.call("ifkv_prompt_attn_partial_tc", N.ptr(qd3), n_qsets, N.ptr(slab_k[li]), N.ptr(slab_v[li]),
                        n_rows, items_p, n_ctx, item_keys, H, Hkv, M, scale, N.ptr(part_ml), N.ptr(part_o), _s())
@@ -527,7 +555,9 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
                 N.call("ifkv_prompt_attn_partial", kv_dt, N.ptr(qd), N.ptr(slab_k[li]), N.ptr(slab_v[li]), N.ptr(kp),
                        N.ptr(vp), items_p, n_ctx, item_keys, H, Hkv, M, Dh, scale, N.ptr(part_ml), N.ptr(part_o),
                        _s())
-            if include_prompt:
+            if side:
+                torch.cuda.current_stream().wait_event(join)
+            elif include_prompt:
                 N.call("ifkv_prompt_attn_partial", kv_dt, N.ptr(qd), N.ptr(slab_k[li]), N.ptr(slab_v[li]), N.ptr(kp),
                        N.ptr(vp), prompt_items_p, n_items - n_ctx, min(M, PROMPT_ITEM_KEYS), H, Hkv, M, Dh, scale,
                        part_ml.data_ptr() + n_ctx * stride_ml, part_o.data_ptr() + n_ctx * stride_o, _s())
