@@ -232,6 +232,14 @@ int ifkv_topk_segments(const float* scores, const int32_t* seg_begin, const int3
 int ifkv_recompute_attn(int dtype, const void* q, const void* k_layer, const void* v_layer,
                         const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows, float scale, void* out,
                         void* stream);
+/* Key ranges instead of prefixes: query row i attends keys key_start[i] ..
+ * horizon[i] (device int64; the block-diagonal causal mask of the batched
+ * chunk prefill, cache.py:74-99 for all chunks in one launch: every chunk's
+ * tokens see only their own chunk).  Tiles are consecutive rows, so
+ * key_start should be non-decreasing for efficiency (not for correctness). */
+int ifkv_recompute_attn_range(int dtype, const void* q, const void* k_layer, const void* v_layer,
+                              const int64_t* key_start, const int64_t* horizon, int S, int H, int Hkv, int Dh,
+                              int n_rows, float scale, void* out, void* stream);
 /* The two implementations behind it (selected automatically): the tcgen05 /
  * TMEM / TMA kernel for bf16, Dh = 128, H/Hkv <= 16; and the generic
  * SIMT fp32-softmax kernel (fp32 mode, other head sizes). */

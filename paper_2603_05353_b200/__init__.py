@@ -20,6 +20,7 @@ from .cache import (
     decode_view,
     full_prefill,
     prefill_chunk,
+    prefill_chunks,
     replace_entries,
     to_decode_layout,
 )

@@ -46,6 +46,7 @@ SIGNATURES = {
     "ifkv_rotate_queries": [P, I32, I32, I32, I32, P, P, I32, P, P, P, P],
     "ifkv_topk_segments": [P, P, P, P, I32, P, I32, P, P],
     "ifkv_recompute_attn": [I32, P, P, P, P, I32, I32, I32, I32, I32, F32, P, P],
+    "ifkv_recompute_attn_range": [I32, P, P, P, P, P, I32, I32, I32, I32, I32, F32, P, P],
     "ifkv_recompute_attn_simt": [I32, P, P, P, P, I32, I32, I32, I32, I32, F32, P, P],
     "ifkv_recompute_attn_tc_supported": [I32, I32, I32, I32],
     "ifkv_recompute_attn_partial": [I32, P, P, P, P, I32, I32, I32, I32, I32, F32, P, P, P],

@@ -321,6 +321,46 @@ def prefill_chunk(weights, chunk: ChunkSpec) -> ChunkKV:
                    np.arange(chunk.local_length, dtype=np.int64), Provenance.PREFILLED_LOCAL, weights.fingerprint())
 
 
+def prefill_chunks(weights, chunks: Sequence[ChunkSpec]) -> List[ChunkKV]:
+    """Chunk-local prefill of many chunks in ONE pass (cache.py:74-99 for
+    every chunk; the role of the reference's thread-pool prefill,
+    costmodel.py:243-270): all tokens go through the layer stack together at
+    their chunk-local positions under a block-diagonal causal mask (token i
+    of a chunk attends rows chunk_start .. i), writing K/V straight into one
+    store slab [L][sum len][Hkv][Dh].  The returned ChunkKVs are views of
+    that store in the given order (each equals ``prefill_chunk`` of its chunk
+    up to the accumulation order).  Batching turns K launches of M = len
+    GEMMs into one launch per projection with M = sum len."""
+    torch = _torch()
+    cfg = weights.config
+    if not chunks:
+        return []
+    for c in chunks:
+        if c.local_length == 0:
+            raise ConfigurationError(f"chunk {c.chunk_id!r} is empty")
+        if c.local_length > cfg.max_position:
+            raise ConfigurationError(f"chunk {c.chunk_id!r} length {c.local_length} exceeds "
+                                     f"max_position {cfg.max_position}")
+    lens = np.array([c.local_length for c in chunks], dtype=np.int64)
+    starts = np.concatenate([[0], np.cumsum(lens)[:-1]])
+    n = int(lens.sum())
+    tok = np.concatenate([np.asarray(c.token_ids, np.int64) for c in chunks])
+    if tok.min() < 0 or tok.max() >= cfg.vocab_size:
+        raise ConfigurationError("token id outside vocabulary")
+    dev = weights.device
+    store_k = torch.empty((cfg.n_layers, n, cfg.kv_heads, cfg.d_head), dtype=weights.torch_dtype, device=dev)
+    store_v = torch.empty_like(store_k)
+    local = np.concatenate([np.arange(m, dtype=np.int64) for m in lens])
+    key_start = np.repeat(starts, lens)
+    rows = torch.arange(n, dtype=torch.int64, device=dev)
+    E.layer_stack(weights, E.h2d(tok, dev), E.h2d(local, dev), store_k, store_v, rows, rows,
+                  key_start=E.h2d(key_start, dev))
+    fp = weights.fingerprint()
+    return [ChunkKV(c.chunk_id, np.asarray(c.token_ids, np.int64).copy(), store_k[:, a:a + m], store_v[:, a:a + m],
+                    np.arange(m, dtype=np.int64), Provenance.PREFILLED_LOCAL, fp)
+            for c, a, m in zip(chunks, starts.tolist(), lens.tolist())]
+
+
 def full_prefill(weights, token_ids, chunk_id: str = "full") -> AssembledCache:
     """The whole context prefilled in one pass at global positions (cache.py:406-425)."""
     tok = np.asarray(token_ids, dtype=np.int64)

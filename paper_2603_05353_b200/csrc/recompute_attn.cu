@@ -13,6 +13,7 @@ constexpr int kRaKeys = 32;    // keys per smem block
 template <typename T>
 __global__ void __launch_bounds__(128) recompute_attn_simt_kernel(const T* __restrict__ q, const T* __restrict__ k,
                                                                   const T* __restrict__ v,
+                                                                  const int64_t* __restrict__ key_start,
                                                                   const int64_t* __restrict__ horizon, int S, int H,
                                                                   int Hkv, int Dh, float scale, T* __restrict__ out,
                                                                   float* __restrict__ ml_out) {
@@ -29,20 +30,25 @@ __global__ void __launch_bounds__(128) recompute_attn_simt_kernel(const T* __res
     Qs[t] = to_f32(q[((int64_t)(t0 + r) * H + h) * Dh + d]);
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int64_t hz[4];
+  int64_t hz[4], ks[4];
   float m[4], l[4], o[4][8];
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     int row = warp * 4 + r;
     hz[r] = row < nt ? horizon[t0 + row] : -1;
+    ks[r] = row < nt && key_start ? key_start[t0 + row] : 0;
     m[r] = -INFINITY;
     l[r] = 0.f;
 #pragma unroll
     for (int u = 0; u < 8; ++u) o[r][u] = 0.f;
   }
   int64_t kmax = -1;  // largest horizon of the tile (-1 in partial mode: no local key visible)
-  for (int r = 0; r < nt; ++r) kmax = max(kmax, horizon[t0 + r]);
-  for (int64_t k0 = 0; k0 <= kmax; k0 += kRaKeys) {
+  int64_t kmin = INT64_MAX;  // smallest first key of the tile (block-diagonal prefill)
+  for (int r = 0; r < nt; ++r) {
+    kmax = max(kmax, horizon[t0 + r]);
+    kmin = min(kmin, key_start ? key_start[t0 + r] : (int64_t)0);
+  }
+  for (int64_t k0 = kmin == INT64_MAX ? 0 : kmin / kRaKeys * kRaKeys; k0 <= kmax; k0 += kRaKeys) {
     __syncthreads();
     const int nk = (int)(kmax + 1 - k0 < kRaKeys ? kmax + 1 - k0 : kRaKeys);
     for (int t = threadIdx.x; t < nk * Dh; t += blockDim.x) {
@@ -54,10 +60,10 @@ __global__ void __launch_bounds__(128) recompute_attn_simt_kernel(const T* __res
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      if (hz[r] < k0) continue;  // warp-uniform
+      if (hz[r] < k0 || k0 + kRaKeys <= ks[r]) continue;  // warp-uniform
       const float* qr = Qs + (warp * 4 + r) * Dh;
       float s = -INFINITY;
-      if (lane < nk && k0 + lane <= hz[r]) {
+      if (lane < nk && k0 + lane <= hz[r] && k0 + lane >= ks[r]) {
         const float* kr = Ks + lane * (Dh + 1);
         float acc = 0.f;
         for (int d = 0; d < Dh; ++d) acc = fmaf(qr[d], kr[d], acc);
@@ -105,8 +111,8 @@ __global__ void __launch_bounds__(128) recompute_attn_simt_kernel(const T* __res
 using namespace ifkv;
 
 extern "C" int ifkv_recompute_attn_tc_v5(const void* q, const void* k_layer, const void* v_layer,
-                                         const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows,
-                                         float scale, void* out, float* ml_out, void* stream);
+                                         const int64_t* key_start, const int64_t* horizon, int S, int H, int Hkv,
+                                         int Dh, int n_rows, float scale, void* out, float* ml_out, void* stream);
 // The tcgen05 kernel (tc_recompute_attn_v5.cu): two ping-ponging tiles per
 // CTA, P staged in smem so S(j+1) follows the read of S(j); tiles of
 // floor(128/G) tokens x G heads; key splits below two waves.  Earlier
@@ -114,13 +120,14 @@ extern "C" int ifkv_recompute_attn_tc_v5(const void* q, const void* k_layer, con
 // measured slower at every C2/C4 grid (profiles/r1_attn_ab.md) and removed.
 static int recompute_attn_tc_any(const void* q, const void* k_layer, const void* v_layer, const int64_t* horizon,
                                  int S, int H, int Hkv, int Dh, int n_rows, float scale, void* out, float* ml_out,
-                                 void* stream) {
-  return ifkv_recompute_attn_tc_v5(q, k_layer, v_layer, horizon, S, H, Hkv, Dh, n_rows, scale, out, ml_out, stream);
+                                 void* stream, const int64_t* key_start = nullptr) {
+  return ifkv_recompute_attn_tc_v5(q, k_layer, v_layer, key_start, horizon, S, H, Hkv, Dh, n_rows, scale, out,
+                                   ml_out, stream);
 }
 
 static int recompute_attn_simt_impl(int dtype, const void* q, const void* k_layer, const void* v_layer,
                                     const int64_t* horizon, int S, int H, int Hkv, int Dh, float scale, void* out,
-                                    float* ml_out, void* stream) {
+                                    float* ml_out, void* stream, const int64_t* key_start = nullptr) {
   IFKV_CHECK_ARG(dtype == IFKV_F32 || dtype == IFKV_BF16, "recompute_attn: bad dtype");
   IFKV_CHECK_ARG(Dh % 2 == 0 && Dh <= 256 && Hkv > 0 && H % Hkv == 0, "recompute_attn: bad shape");
   if (S <= 0) return IFKV_OK;
@@ -130,13 +137,13 @@ static int recompute_attn_simt_impl(int dtype, const void* q, const void* k_laye
     auto kern = recompute_attn_simt_kernel<__nv_bfloat16>;
     IFKV_CUDA_CALL(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "recompute_attn");
     kern<<<grid, 128, sm, as_stream(stream)>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k_layer,
-                                               (const __nv_bfloat16*)v_layer, horizon, S, H, Hkv, Dh, scale,
+                                               (const __nv_bfloat16*)v_layer, key_start, horizon, S, H, Hkv, Dh, scale,
                                                (__nv_bfloat16*)out, ml_out);
   } else {
     auto kern = recompute_attn_simt_kernel<float>;
     IFKV_CUDA_CALL(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "recompute_attn");
-    kern<<<grid, 128, sm, as_stream(stream)>>>((const float*)q, (const float*)k_layer, (const float*)v_layer, horizon,
-                                               S, H, Hkv, Dh, scale, (float*)out, ml_out);
+    kern<<<grid, 128, sm, as_stream(stream)>>>((const float*)q, (const float*)k_layer, (const float*)v_layer, key_start,
+                                               horizon, S, H, Hkv, Dh, scale, (float*)out, ml_out);
   }
   IFKV_LAUNCH_CHECK("recompute_attn_simt");
   return IFKV_OK;
@@ -146,6 +153,17 @@ extern "C" int ifkv_recompute_attn_simt(int dtype, const void* q, const void* k_
                                         const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows, float scale,
                                         void* out, void* stream) {
   return recompute_attn_simt_impl(dtype, q, k_layer, v_layer, horizon, S, H, Hkv, Dh, scale, out, nullptr, stream);
+}
+
+extern "C" int ifkv_recompute_attn_range(int dtype, const void* q, const void* k_layer, const void* v_layer,
+                                         const int64_t* key_start, const int64_t* horizon, int S, int H, int Hkv,
+                                         int Dh, int n_rows, float scale, void* out, void* stream) {
+  IFKV_CHECK_ARG(key_start != nullptr, "recompute_attn_range: key_start required");
+  if (ifkv_recompute_attn_tc_supported(dtype, H, Hkv, Dh))
+    return recompute_attn_tc_any(q, k_layer, v_layer, horizon, S, H, Hkv, Dh, n_rows, scale, out, nullptr, stream,
+                                 key_start);
+  return recompute_attn_simt_impl(dtype, q, k_layer, v_layer, horizon, S, H, Hkv, Dh, scale, out, nullptr, stream,
+                                  key_start);
 }
 
 extern "C" int ifkv_recompute_attn(int dtype, const void* q, const void* k_layer, const void* v_layer,
@@ -231,7 +249,7 @@ extern "C" int ifkv_recompute_attn_partial(int dtype, const void* q, const void*
                                            const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows,
                                            float scale, void* out, float* ml_out, void* stream) {
   IFKV_CHECK_ARG(ml_out != nullptr, "recompute_attn_partial: ml_out required");
-  if (n_rows <= 0) return IFKV_ERR_ARG;
+  IFKV_CHECK_ARG(n_rows > 0, "recompute_attn_partial: the shard holds no key rows (n_rows = %d)", n_rows);
   if (ifkv_recompute_attn_tc_supported(dtype, H, Hkv, Dh))
     return recompute_attn_tc_any(q, k_layer, v_layer, horizon, S, H, Hkv, Dh, n_rows, scale, out, ml_out, stream);
   return recompute_attn_simt_impl(dtype, q, k_layer, v_layer, horizon, S, H, Hkv, Dh, scale, out, ml_out, stream);

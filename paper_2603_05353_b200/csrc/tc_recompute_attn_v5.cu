@@ -57,6 +57,7 @@ struct Smem {
   uint64_t s_full[2], s_free[2], p_full[2][2], pv_done[2][2], o_final[2];
   uint32_t tmem_base;
   int n_blocks[2];
+  int first_block;
 };
 
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
@@ -80,6 +81,16 @@ __device__ __forceinline__ int tile_blocks_warp(const int64_t* horizon, int t0, 
   for (int o = 16; o > 0; o >>= 1) mx = max(mx, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)mx, o));
   return mx < 0 ? 0 : (int)((mx + kKeys) / kKeys);
 }
+// First key block any token of the tile can see (key ranges key_start..horizon;
+// key_start == nullptr: every range starts at key 0).
+__device__ __forceinline__ int tile_first_block_warp(const int64_t* key_start, int t0, int tok, int S) {
+  if (key_start == nullptr) return 0;
+  int64_t mn = INT64_MAX;
+  for (int t = t0 + (threadIdx.x & 31); t < min(t0 + tok, S); t += 32) mn = min(mn, key_start[t]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mn = min(mn, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)mn, o));
+  return mn == INT64_MAX ? 0 : (int)(mn / kKeys);
+}
 
 // 8 bf16 (16 B chunk c of a 64-key panel) of row r into the swizzled P tile.
 __device__ __forceinline__ void st_p_chunk(uint8_t* p, int r, int panel, int c, uint4 v) {
@@ -88,7 +99,7 @@ __device__ __forceinline__ void st_p_chunk(uint8_t* p, int r, int panel, int c, 
 
 __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int nblk, int b0, int t0, int S, int H,
                                              int G, int Gp, int g, const int64_t* __restrict__ horizon,
-                                             float scale_log2,
+                                             const int64_t* __restrict__ key_start, float scale_log2,
                                              __nv_bfloat16* __restrict__ out, float* __restrict__ ml_out) {
   const int w = (threadIdx.x >> 5) & 3;
   const int lane = threadIdx.x & 31;
@@ -98,6 +109,7 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
   const int tok = t0 + row / Gp;
   const bool valid = row < (kRows / Gp) * Gp && row % Gp < G && tok < S;  // tile rows: tokens x Gp heads
   const int hz = valid ? (int)horizon[tok] : INT_MAX;  // pad rows: never force the masked path
+  const int ks = valid && key_start ? (int)key_start[tok] : 0;  // first visible key (block-diagonal prefill)
   const uint32_t lane_off = (uint32_t)(w * 32) << 16;
   const uint32_t t_s = tmem + 256 * x + lane_off;
   const uint32_t t_o = t_s + 128;
@@ -107,7 +119,7 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
     tc::mbar_wait(&sm.s_full[x], j & 1);
     tc::tc_fence_after();
     const int j0 = (b0 + j) * kKeys;
-    const bool masked = __any_sync(0xffffffffu, j0 + kKeys - 1 > hz);
+    const bool masked = __any_sync(0xffffffffu, j0 + kKeys - 1 > hz || j0 < ks);
 #if IFKV_ATTN5_ONEPASS
     // one TMEM read of the whole S row; S_x(j+1) may start right after it
     float v[128];
@@ -186,7 +198,7 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
       if (masked) {
 #pragma unroll
         for (int c = 0; c < 64; ++c)
-          if (j0 + hf * 64 + c > hz) v[c] = -INFINITY;
+          if (j0 + hf * 64 + c > hz || j0 + hf * 64 + c < ks) v[c] = -INFINITY;
       }
 #pragma unroll
       for (int c = 0; c < 64; c += 2) mx = tc::max3(mx, v[c], v[c + 1]);
@@ -233,7 +245,7 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
       if (masked) {
 #pragma unroll
         for (int c = 0; c < 64; ++c)
-          if (j0 + hf * 64 + c > hz) v[c] = -INFINITY;
+          if (j0 + hf * 64 + c > hz || j0 + hf * 64 + c < ks) v[c] = -INFINITY;
       }
       float2 sum2 = make_float2(0.f, 0.f);
 #pragma unroll
@@ -303,7 +315,8 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
 
 __global__ void __launch_bounds__(384, 1)
     recompute_attn_v5_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                             const __grid_constant__ CUtensorMap tm_v, const int64_t* __restrict__ horizon, int S,
+                             const __grid_constant__ CUtensorMap tm_v, const int64_t* __restrict__ horizon,
+                             const int64_t* __restrict__ key_start, int S,
                              int H, int Hkv, int Gp, float scale_log2, __nv_bfloat16* __restrict__ out,
                              float* __restrict__ ml_out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -317,9 +330,12 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 3) {
     const int a = tA < S ? tile_blocks_warp(horizon, tA, tok, S) : 0;
     const int b = tB < S ? tile_blocks_warp(horizon, tB, tok, S) : 0;
+    const int fa = tA < S ? tile_first_block_warp(key_start, tA, tok, S) : INT_MAX;
+    const int fb = tB < S ? tile_first_block_warp(key_start, tB, tok, S) : INT_MAX;
     if (lane == 0) {
       sm.n_blocks[0] = a;
       sm.n_blocks[1] = b;
+      sm.first_block = min(min(fa, fb), max(a, b));  // blocks before it are masked for every row
     }
   }
   if (threadIdx.x == 0) {
@@ -356,8 +372,9 @@ __global__ void __launch_bounds__(384, 1)
   tc::tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
   const int n_full = max(sm.n_blocks[0], sm.n_blocks[1]);
-  const int b0 = (int)((int64_t)blockIdx.z * n_full / gridDim.z);
-  const int b1 = (int)((int64_t)(blockIdx.z + 1) * n_full / gridDim.z);
+  const int kb0 = sm.first_block;  // key ranges: blocks [kb0, n_full)
+  const int b0 = kb0 + (int)((int64_t)blockIdx.z * (n_full - kb0) / gridDim.z);
+  const int b1 = kb0 + (int)((int64_t)(blockIdx.z + 1) * (n_full - kb0) / gridDim.z);
   const int nA = max(0, min(sm.n_blocks[0], b1) - b0), nB = max(0, min(sm.n_blocks[1], b1) - b0);
   const int nblk = max(nA, nB);
   out += (int64_t)blockIdx.z * S * H * kDh;
@@ -530,7 +547,7 @@ __global__ void __launch_bounds__(384, 1)
     const int x = (warp - 4) >> 2;
     const int nx = x == 0 ? nA : nB;
     const int tx = x == 0 ? tA : tB;
-    if (tx < S) softmax_tile(sm, tmem, x, nx, b0, tx, S, H, G, Gp, g, horizon, scale_log2, out, ml_out);
+    if (tx < S) softmax_tile(sm, tmem, x, nx, b0, tx, S, H, G, Gp, g, horizon, key_start, scale_log2, out, ml_out);
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -582,8 +599,8 @@ extern "C" int ifkv_recompute_attn_tc_supported(int dtype, int H, int Hkv, int D
 }
 
 extern "C" int ifkv_recompute_attn_tc_v5(const void* q, const void* k_layer, const void* v_layer,
-                                         const int64_t* horizon, int S, int H, int Hkv, int Dh, int n_rows,
-                                         float scale, void* out, float* ml_out, void* stream) {
+                                         const int64_t* key_start, const int64_t* horizon, int S, int H, int Hkv,
+                                         int Dh, int n_rows, float scale, void* out, float* ml_out, void* stream) {
   IFKV_CHECK_ARG(Dh == kDh && Hkv > 0 && H % Hkv == 0 && H / Hkv <= 16, "recompute_attn_v5: unsupported shape");
   if (S <= 0) return IFKV_OK;
   const int G = H / Hkv;
@@ -630,7 +647,7 @@ extern "C" int ifkv_recompute_attn_tc_v5(const void* q, const void* k_layer, con
     P = min(IFKV_ATTN5_SPLIT_MAX, (IFKV_ATTN5_SPLIT_WAVES * sms + Hkv * pairs - 1) / (Hkv * pairs));
 #endif
   if (P == 1) {
-    recompute_attn_v5_kernel<<<dim3(Hkv, pairs, 1), 384, smem, st>>>(tq, tk, tv, horizon, S, H, Hkv, Gp,
+    recompute_attn_v5_kernel<<<dim3(Hkv, pairs, 1), 384, smem, st>>>(tq, tk, tv, horizon, key_start, S, H, Hkv, Gp,
                                                                      scale_log2, (__nv_bfloat16*)out, ml_out);
     IFKV_LAUNCH_CHECK("recompute_attn_v5");
     return IFKV_OK;
@@ -645,7 +662,7 @@ extern "C" int ifkv_recompute_attn_tc_v5(const void* q, const void* k_layer, con
   }
   auto* part_o = reinterpret_cast<__nv_bfloat16*>(ws);
   auto* part_ml = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + o_bytes);
-  recompute_attn_v5_kernel<<<dim3(Hkv, pairs, P), 384, smem, st>>>(tq, tk, tv, horizon, S, H, Hkv, Gp, scale_log2,
+  recompute_attn_v5_kernel<<<dim3(Hkv, pairs, P), 384, smem, st>>>(tq, tk, tv, horizon, key_start, S, H, Hkv, Gp, scale_log2,
                                                                    part_o, part_ml);
   IFKV_LAUNCH_CHECK("recompute_attn_v5 (split)");
   attn_v5_merge_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(part_o, part_ml, P, rows, (__nv_bfloat16*)out,

@@ -253,12 +253,17 @@ def merge_prompt_states(parts_ctx, parts_ml):
     return ctx, ml
 
 
-def recompute_attn(q, k_layer, v_layer, horizon, H, Hkv, Dh, out=None, impl: str = "auto"):
-    """impl: "auto" (tcgen05 when supported, else SIMT) or "simt"."""
+def recompute_attn(q, k_layer, v_layer, horizon, H, Hkv, Dh, out=None, impl: str = "auto", key_start=None):
+    """impl: "auto" (tcgen05 when supported, else SIMT) or "simt".
+    ``key_start`` (device int64, optional): rows attend keys key_start..horizon."""
     torch = _torch()
     S = q.shape[0]
     if out is None:
         out = torch.empty_like(q)
+    if key_start is not None:
+        N.call("ifkv_recompute_attn_range", dt_code(q), N.ptr(q), N.ptr(k_layer), N.ptr(v_layer), N.ptr(key_start),
+               N.ptr(horizon), S, H, Hkv, Dh, k_layer.shape[0], 1.0 / math.sqrt(Dh), N.ptr(out), _s())
+        return out
     name = "ifkv_recompute_attn" if impl == "auto" else "ifkv_recompute_attn_simt"
     N.call(name, dt_code(q), N.ptr(q), N.ptr(k_layer), N.ptr(v_layer), N.ptr(horizon), S, H, Hkv, Dh,
            k_layer.shape[0], 1.0 / math.sqrt(Dh), N.ptr(out), _s())
@@ -608,13 +613,15 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
 
 
 def layer_stack(weights, token_ids, positions, k_slab, v_slab, dst_rows, horizon, want_hidden: bool = False,
-                attn_fn=None, n_layers: Optional[int] = None, on_hidden=None):
+                attn_fn=None, n_layers: Optional[int] = None, on_hidden=None, key_start=None):
     """Advance S tokens (device int64 ids/positions) through every layer
     (or the first ``n_layers``).
 
     Layer l: x = rms_norm(h); q,k,v = x W; rope at ``positions``; k,v written
     to slab rows ``dst_rows`` (so later tokens see them); attention of q over
-    slab keys 0..horizon[i]; residual O-proj and MLP.  The last layer stops
+    slab keys 0..horizon[i] (key_start[i]..horizon[i] when given: the
+    block-diagonal mask of the batched chunk prefill); residual O-proj and
+    MLP.  The last layer stops
     after its K/V (nothing else can change a K/V row) unless the hidden state
     is wanted; ``on_hidden(l, h)`` sees each layer's block output (fp32 [S, d],
     model.py:450-452).
@@ -661,7 +668,7 @@ def layer_stack(weights, token_ids, positions, k_slab, v_slab, dst_rows, horizon
             attn_out = attn_fn(li, qbuf, k_slab[li], v_slab[li])
         else:
             with _Bracket("recompute_attn", li):
-                recompute_attn(qbuf, k_slab[li], v_slab[li], horizon, H, Hkv, Dh, out=attn_out)
+                recompute_attn(qbuf, k_slab[li], v_slab[li], horizon, H, Hkv, Dh, out=attn_out, key_start=key_start)
         gemm(attn_out.view(S, d), lw.wo, out=h, accumulate=True)  # h += ctx Wo
         x2 = add_rmsnorm(h, None, 0, lw.mlp_norm, act_mode)
         if fused_mlp:

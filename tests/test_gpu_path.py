@@ -329,3 +329,37 @@ def test_cacheblend_validation(tiny):
         P.score_cacheblend(dw, [], 1)
     s = P.score_cacheblend(dw, chunks, 2).cpu().numpy()
     np.testing.assert_array_equal(s, np.zeros(5))
+
+
+# ---------------------------------------------------------------------------
+# batched chunk prefill (cache.py:74-99 for many chunks in one layer stack)
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("precision,cfg_name", [("bf16", "c1"), ("bf16", "gqa7"), ("f32", "c1")])
+def test_prefill_chunks_matches_oracle_per_chunk(cuda, precision, cfg_name):
+    """One block-diagonal layer stack over ragged chunks (lengths not multiples
+    of the 32-token / 18-token attention tiles, a 1-token chunk) equals the
+    oracle's per-chunk prefill, and the per-chunk GPU prefill."""
+    P = _pkg()
+    if cfg_name == "c1":
+        cfg = P.c1_config()
+    else:  # GQA group 7 (Qwen2.5-VL-like tiles of 18 tokens x 7 heads)
+        cfg = P.ModelConfig(n_layers=2, n_heads=14, d_model=1792, d_head=128, d_ff=512, vocab_size=512,
+                            max_position=8192, n_kv_heads=2)
+    dw, ow, _ = _setup(cfg, 7, precision, None, 0)
+    rng = np.random.default_rng(1)
+    lens = [100, 37, 300, 1, 64, 256]
+    chunks = [P.ChunkSpec(f"c{i}", rng.integers(0, cfg.vocab_size, size=n)) for i, n in enumerate(lens)]
+    got = P.prefill_chunks(dw, chunks)
+    tol = 1e-2 if precision == "bf16" else 1e-4
+    for ckv, spec in zip(got, chunks):
+        want = O.prefill_chunk(ow, spec.chunk_id, spec.token_ids)
+        assert rel_err(to_np(ckv.keys), want.keys) <= tol
+        assert rel_err(to_np(ckv.values), want.values) <= tol
+        one = P.prefill_chunk(dw, spec)
+        assert rel_err(to_np(ckv.keys), to_np(one.keys)) <= tol
+        np.testing.assert_array_equal(ckv.prefill_positions, np.arange(spec.local_length))
+    # the batched store feeds the path like separately prefilled chunks
+    cache = P.assemble(got)
+    assert cache.context_length == sum(lens)
