@@ -30,6 +30,7 @@ SIGNATURES = {
     "ifkv_rope_table": [P, I32, I32, F64, P, P],
     "ifkv_rotate_rows": [I32, P, P, I64, I32, I32, I32, I32, P, P, P],
     "ifkv_assemble_gather": [I32, I32, P, P, P, P, P, P, P, I64, I32, I32, P],
+    "ifkv_assemble_gather_rotate": [I32, I32, P, P, P, P, P, P, P, I32, P, P, I64, I32, I32, P],
     "ifkv_add_rmsnorm": [P, P, I32, I32, P, I32, I32, I32, P, P],
     "ifkv_silu_mul": [P, I32, I32, I32, I32, I32, I32, P, P],
     "ifkv_embed_rows": [P, I32, P, I32, I32, P, P],

@@ -50,6 +50,11 @@ class ChunkKV:
     prefill_positions: np.ndarray
     provenance: Provenance
     model_fingerprint: int
+    # set by prefill_chunks: (store_k, store_v) this chunk is a row range of,
+    # and its first store row -- lets the query path score straight from the
+    # store and assemble with the rotation fused (pipeline.py)
+    store: Optional[tuple] = field(default=None, repr=False, compare=False)
+    store_row0: int = -1
 
     def __post_init__(self):
         self.token_ids = np.asarray(self.token_ids, dtype=np.int64)
@@ -181,6 +186,81 @@ def assemble(chunks: Sequence[ChunkKV], prompt_kv: Optional[PromptKV] = None) ->
         chunk_index=parts([np.full(n, i, np.int64) for i, n in enumerate(lens)], np.int64),
         local_index=parts([np.arange(n, dtype=np.int64) for n in lens], np.int64),
         prompt_length=m,
+        model_fingerprint=fp,
+    )
+
+
+def assemble_decode_layout(chunks: Sequence[ChunkKV], rope_base: float, stream=None) -> AssembledCache:
+    """``assemble`` and Kernel 1 in one pass: the chunks gathered in declared
+    order with every key rotated from its stored position to its assembled
+    (global) position while it is copied (``ifkv_assemble_gather_rotate``),
+    i.e. ``to_decode_layout(assemble(chunks))`` with one read and one write
+    of K instead of two of each.  Enqueued on ``stream`` (default: current)."""
+    torch = _torch()
+    if not chunks:
+        raise ConfigurationError("nothing to assemble: no chunks")
+    base = assemble_metadata(chunks)
+    ref = chunks[0].keys
+    L, _, Hkv, Dh = ref.shape
+    n = base.context_length
+    keys = torch.empty((L, n, Hkv, Dh), dtype=ref.dtype, device=ref.device)
+    values = torch.empty_like(keys)
+    starts = np.concatenate([[0], np.cumsum(base.chunk_lengths)[:-1]]).astype(np.int64)
+    deltas = starts - np.array([int(c.prefill_positions[0]) for c in chunks], dtype=np.int64)
+    uniq = sorted({int(d) for d in deltas if d != 0})
+    cs_row = [uniq.index(int(d)) if d != 0 else -1 for d in deltas]
+    # every chunk's stored positions must be one consecutive run (true for prefilled chunks)
+    for c in chunks:
+        if c.length and not np.array_equal(c.prefill_positions, c.prefill_positions[0] + np.arange(c.length)):
+            raise ConfigurationError(f"chunk {c.chunk_id!r}: stored positions are not one run")
+    cs = E.rope_table(np.asarray(uniq or [0], np.int64), Dh, rope_base, ref.device)
+    if stream is not None:  # the gather may overlap later work of the current stream
+        stream.wait_stream(torch.cuda.current_stream())
+        for t in (cs, keys, values):  # used on the side stream: no reuse before its work is done
+            t.record_stream(stream)
+    with (torch.cuda.stream(stream) if stream is not None else _nullctx()):
+        E.assemble_gather([c.keys for c in chunks], [c.values for c in chunks], keys, values, starts.tolist(),
+                          cs_row=cs_row, cs=cs)
+    base.keys, base.values = keys, values
+    base.row_positions = np.concatenate([starts[i] + np.arange(c.length) for i, c in enumerate(chunks)])
+    base.row_positions = base.row_positions.astype(np.int64)
+    return base
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def assemble_metadata(chunks: Sequence[ChunkKV]) -> AssembledCache:
+    """The host-side bookkeeping of ``assemble`` (checks, token ids, row
+    positions, provenance, chunk mapping) with no device slab."""
+    if not chunks:
+        raise ConfigurationError("nothing to assemble: no chunks")
+    fp = chunks[0].model_fingerprint
+    ref = chunks[0].keys
+    for c in chunks:
+        if c.model_fingerprint != fp:
+            raise ConfigurationError(f"chunk {c.chunk_id!r} was prefetched under a different model "
+                                     f"(fingerprint {c.model_fingerprint:#x} != {fp:#x})")
+        if c.n_layers != ref.shape[0] or c.keys.shape[2:] != ref.shape[2:] or c.keys.dtype != ref.dtype:
+            raise ConfigurationError(f"chunk {c.chunk_id!r} KV shape mismatch")
+    lens = [c.length for c in chunks]
+    cat = lambda xs, dt: np.concatenate(xs).astype(dt) if xs else np.zeros(0, dt)  # noqa: E731
+    return AssembledCache(
+        chunk_ids=[c.chunk_id for c in chunks],
+        chunk_lengths=lens,
+        token_ids=cat([c.token_ids for c in chunks], np.int64),
+        keys=None,
+        values=None,
+        row_positions=cat([c.prefill_positions for c in chunks], np.int64),
+        provenance=cat([np.full(c.length, int(c.provenance), np.uint8) for c in chunks], np.uint8),
+        chunk_index=cat([np.full(n, i, np.int64) for i, n in enumerate(lens)], np.int64),
+        local_index=cat([np.arange(n, dtype=np.int64) for n in lens], np.int64),
+        prompt_length=0,
         model_fingerprint=fp,
     )
 
@@ -356,8 +436,9 @@ def prefill_chunks(weights, chunks: Sequence[ChunkSpec]) -> List[ChunkKV]:
     E.layer_stack(weights, E.h2d(tok, dev), E.h2d(local, dev), store_k, store_v, rows, rows,
                   key_start=E.h2d(key_start, dev))
     fp = weights.fingerprint()
+    store = (store_k, store_v)
     return [ChunkKV(c.chunk_id, np.asarray(c.token_ids, np.int64).copy(), store_k[:, a:a + m], store_v[:, a:a + m],
-                    np.arange(m, dtype=np.int64), Provenance.PREFILLED_LOCAL, fp)
+                    np.arange(m, dtype=np.int64), Provenance.PREFILLED_LOCAL, fp, store=store, store_row0=a)
             for c, a, m in zip(chunks, starts.tolist(), lens.tolist())]
 
 

@@ -75,6 +75,13 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
+// RoPE rotation of one interleaved pair by (cos, sin) = c, with a fixed
+// rounding sequence (x0 c - x1 s as fmul + fma) so that every kernel that moves
+// a stored key (Kernel 1, the rotating gather) produces identical bits.
+__device__ __forceinline__ float2 rot_pair(float x0, float x1, float2 c) {
+  return make_float2(__fmaf_rn(x0, c.x, -__fmul_rn(x1, c.y)), __fmaf_rn(x0, c.y, __fmul_rn(x1, c.x)));
+}
+
 // Split an fp32 value into three bf16 terms whose sum reproduces it to
 // ~2^-24 relative: hi = rn(x), mid = rn(x - hi), lo = rn(x - hi - mid).
 __device__ __forceinline__ void split3(float x, __nv_bfloat16& hi, __nv_bfloat16& mid, __nv_bfloat16& lo) {

@@ -71,9 +71,9 @@ __global__ void __launch_bounds__(256) rotate_rows_kernel(const T* __restrict__ 
           T* e = reinterpret_cast<T*>(&val[q][u]);
 #pragma unroll
           for (int p = 0; p < kPairs; ++p) {
-            float x0 = to_f32(e[2 * p]), x1 = to_f32(e[2 * p + 1]);
-            e[2 * p] = from_f32<T>(x0 * c[p].x - x1 * c[p].y);
-            e[2 * p + 1] = from_f32<T>(x0 * c[p].y + x1 * c[p].x);
+            const float2 y = rot_pair(to_f32(e[2 * p]), to_f32(e[2 * p + 1]), c[p]);
+            e[2 * p] = from_f32<T>(y.x);
+            e[2 * p + 1] = from_f32<T>(y.y);
           }
         }
       }
@@ -82,135 +82,6 @@ __global__ void __launch_bounds__(256) rotate_rows_kernel(const T* __restrict__ 
         *reinterpret_cast<uint4*>(dst + base[q] + (int64_t)(lane + 32 * u) * kVec) = val[q][u];
     }
   }
-}
-
-// TMA-staged Kernel 1 (bf16, in place; A/B variant, see IFKV_ROT_TMA):
-// persistent CTAs walk 16/32-row units
-// (layer, rows [32u, 32u + 32)); thread 0 moves each unit HBM -> smem with one
-// cp.async.bulk (mbarrier complete_tx), all threads rotate it in smem with
-// 16-byte accesses, and thread 0 writes it back with one bulk store.  Three
-// 64 KB stages: the load of unit i+2 and the store of unit i-1 overlap the
-// rotation of unit i.  Units with no moved row are skipped (no traffic);
-// unmoved rows inside a mixed unit are written back unchanged (bit-exact).
-#ifndef IFKV_ROT_ROWS
-#define IFKV_ROT_ROWS 16
-#endif
-#ifndef IFKV_ROT_STAGES
-#define IFKV_ROT_STAGES 6
-#endif
-constexpr int kRotRows = IFKV_ROT_ROWS;  // <= 32 (one warp lane per row in the unit scan)
-constexpr int kRotStages = IFKV_ROT_STAGES;
-
-__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   (uint32_t)__cvta_generic_to_shared(smem)),
-               "l"(gmem), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
-               : "memory");
-}
-__device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem),
-               "r"((uint32_t)__cvta_generic_to_shared(smem)), "r"(bytes)
-               : "memory");
-}
-
-__global__ void __launch_bounds__(256, 1) rotate_rows_tma_kernel(__nv_bfloat16* __restrict__ slab,
-                                                                 int64_t layer_stride, int n_rows, int n_layers,
-                                                                 int row_vecs, int vecs_per_head,
-                                                                 const int32_t* __restrict__ row_table,
-                                                                 const float2* __restrict__ cs, int half) {
-  extern __shared__ __align__(128) uint8_t rot_smem[];
-  const int row_bytes = row_vecs * 16;
-  uint8_t* stage = rot_smem;
-  uint64_t* full = reinterpret_cast<uint64_t*>(rot_smem + kRotStages * kRotRows * row_bytes);
-  int* unit_of = reinterpret_cast<int*>(full + kRotStages);
-  const int units_per_layer = (n_rows + kRotRows - 1) / kRotRows;
-  const int n_units = units_per_layer * n_layers;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kRotStages; ++i)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(full + i)));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  // warp 0: next unit of this CTA that has a moved row (or n_units: none);
-  // one lane per row of the unit, ballot
-  int next_u = blockIdx.x;
-  const int lane = threadIdx.x & 31;
-  auto find = [&](int u) {
-    for (; u < n_units; u += gridDim.x) {
-      const int r = (u % units_per_layer) * kRotRows + lane;
-      const bool moved = lane < kRotRows && r < n_rows && row_table[r] >= 0;
-      if (__any_sync(0xffffffffu, moved)) return u;
-    }
-    return n_units;
-  };
-  auto issue = [&](int i, int u) {  // unit u into stage i % kRotStages (thread 0)
-    const int st = i % kRotStages;
-    unit_of[st] = u;
-    if (u >= n_units) {
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((uint32_t)__cvta_generic_to_shared(full + st))
-                   : "memory");
-      return;
-    }
-    const int layer = u / units_per_layer, r0 = (u % units_per_layer) * kRotRows;
-    const uint32_t bytes = (uint32_t)(min(kRotRows, n_rows - r0) * row_bytes);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                     (uint32_t)__cvta_generic_to_shared(full + st)),
-                 "r"(bytes)
-                 : "memory");
-    bulk_g2s(stage + st * kRotRows * row_bytes, slab + layer * layer_stride + (int64_t)r0 * row_vecs * 8, bytes,
-             full + st);
-  };
-  if (threadIdx.x < 32) {
-    for (int i = 0; i < kRotStages - 1; ++i) {
-      next_u = find(next_u);
-      if (lane == 0) issue(i, next_u);
-      if (next_u < n_units) next_u += gridDim.x;
-    }
-  }
-  for (int i = 0;; ++i) {
-    const int st = i % kRotStages;
-    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(full + st), par = (i / kRotStages) & 1;
-    asm volatile(
-        "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(
-            bar),
-        "r"(par)
-        : "memory");
-    const int u = unit_of[st];
-    if (u >= n_units) break;
-    const int r0 = (u % units_per_layer) * kRotRows;
-    const int rows = min(kRotRows, n_rows - r0);
-    uint4* sv = reinterpret_cast<uint4*>(stage + st * kRotRows * row_bytes);
-    for (int v = threadIdx.x; v < rows * row_vecs; v += blockDim.x) {
-      const int rr = v / row_vecs;
-      const int tab = row_table[r0 + rr];
-      if (tab < 0) continue;
-      uint4 val = sv[v];
-      const float2* c = cs + (int64_t)tab * half + ((v - rr * row_vecs) % vecs_per_head) * 4;
-      __nv_bfloat162* e = reinterpret_cast<__nv_bfloat162*>(&val);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float2 a = __ldg(c + q);
-        const float2 x = __bfloat1622float2(e[q]);
-        e[q] = __floats2bfloat162_rn(x.x * a.x - x.y * a.y, x.x * a.y + x.y * a.x);
-      }
-      sv[v] = val;
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      if (lane == 0) {
-        const int layer = u / units_per_layer;
-        bulk_s2g(slab + layer * layer_stride + (int64_t)r0 * row_vecs * 8, sv, (uint32_t)(rows * row_bytes));
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        // the next unit's stage was last used by unit i - 1: its store must have read it
-        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-      }
-      next_u = find(next_u);
-      if (lane == 0) issue(i + kRotStages - 1, next_u);
-      if (next_u < n_units) next_u += gridDim.x;
-    }
-  }
-  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // Generic fallback: one thread per 16-byte vector (rows not a multiple of
@@ -602,24 +473,6 @@ extern "C" int ifkv_rotate_rows(int dtype, const void* src, void* dst, int64_t l
   auto tab = reinterpret_cast<const float2*>(cs);
   cudaStream_t st = as_stream(stream);
   const int64_t rows = (int64_t)n_layers * n_rows;
-// TMA-staged variant (A/B only): measured 3.5 TB/s vs 5.5 TB/s for the
-// register-path kernel below (tools/rot_bench.py, C2 slab) -- the per-unit
-// CTA-wide barrier serialises the staging; the register path keeps four
-// 16-byte loads per thread and eight CTAs per SM in flight instead.
-#ifndef IFKV_ROT_TMA
-#define IFKV_ROT_TMA 0
-#endif
-  const size_t tma_smem = (size_t)kRotStages * kRotRows * vecs_per_row * 16 + kRotStages * (8 + 4) + 16;
-  if (IFKV_ROT_TMA && in_place && dtype == IFKV_BF16 && tma_smem <= 200 * 1024 &&
-      (layer_stride * 2) % 16 == 0) {
-    IFKV_CUDA_CALL(cudaFuncSetAttribute(rotate_rows_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)tma_smem),
-                   "rotate_rows: smem attribute");
-    rotate_rows_tma_kernel<<<sms, 256, tma_smem, st>>>((__nv_bfloat16*)dst, layer_stride, n_rows, n_layers,
-                                                       vecs_per_row, vecs_per_head, row_table, tab, d_head / 2);
-    IFKV_LAUNCH_CHECK("rotate_rows_tma");
-    return IFKV_OK;
-  }
   const bool warp_rows = vecs_per_row % 32 == 0 && 32 % vecs_per_head == 0 && vecs_per_row / 32 <= 8;
   if (warp_rows) {
     const int64_t want = (rows + 15) / 16;  // 8 warps x 2 rows per CTA iteration

@@ -118,7 +118,11 @@ def rotate_rows(src, dst, row_table, cs):
     return dst
 
 
-def assemble_gather(src_keys: Sequence, src_values: Sequence, dst_k, dst_v, row0: Sequence[int]):
+def assemble_gather(src_keys: Sequence, src_values: Sequence, dst_k, dst_v, row0: Sequence[int], cs_row=None,
+                    cs=None):
+    """Gather chunk K/V into slab rows row0[c] ..; with ``cs_row``/``cs``
+    (per-chunk row of a (cos, sin) table, -1 = none) the keys are rotated
+    while copied (ifkv_assemble_gather_rotate)."""
     import ctypes as C
 
     n = len(src_keys)
@@ -136,9 +140,17 @@ def assemble_gather(src_keys: Sequence, src_values: Sequence, dst_k, dst_v, row0
                 raise ConfigurationError("chunk KV rows must be contiguous [L, len, Hkv, Dh] of the slab dtype")
         if tk.stride(0) != tv.stride(0):
             raise ConfigurationError("chunk keys and values must share a layer stride")
-    N.call("ifkv_assemble_gather", dt_code(dst_k), n, C.cast(pk, C.c_void_p), C.cast(pv, C.c_void_p),
-           C.cast(strides, C.c_void_p), C.cast(lens, C.c_void_p), C.cast(r0, C.c_void_p), N.ptr(dst_k),
-           N.ptr(dst_v), dst_k.stride(0), L, Hkv * Dh, _s())
+    if cs_row is None:
+        N.call("ifkv_assemble_gather", dt_code(dst_k), n, C.cast(pk, C.c_void_p), C.cast(pv, C.c_void_p),
+               C.cast(strides, C.c_void_p), C.cast(lens, C.c_void_p), C.cast(r0, C.c_void_p), N.ptr(dst_k),
+               N.ptr(dst_v), dst_k.stride(0), L, Hkv * Dh, _s())
+        return
+    crow = (C.c_int32 * n)(*[int(x) for x in cs_row])
+    with _Bracket("assemble_rotate", 4 * sum(t.shape[1] for t in src_keys) * L * Hkv * Dh * dst_k.element_size()):
+        N.call("ifkv_assemble_gather_rotate", dt_code(dst_k), n, C.cast(pk, C.c_void_p), C.cast(pv, C.c_void_p),
+               C.cast(strides, C.c_void_p), C.cast(lens, C.c_void_p), C.cast(r0, C.c_void_p),
+               C.cast(crow, C.c_void_p), N.ptr(cs), Dh, N.ptr(dst_k), N.ptr(dst_v), dst_k.stride(0), L, Hkv * Dh,
+               _s())
 
 
 def add_rmsnorm(h, delta, n_parts: int, gain, out_mode: int):
@@ -284,14 +296,17 @@ _SMS: List[int] = []
 _SIDE: dict = {}
 
 
-def _side_stream():
-    """A second stream per device for work that can overlap the current
-    stream's kernels (fork/join through events)."""
+def _side_stream(idx: int = 0):
+    """Side streams per device for work that can overlap the current
+    stream's kernels (fork/join through events): 0 = the scoring pass's
+    prompt items (high priority), 1 = unused, 2 = the scoring pass itself
+    (high priority, so its CTAs are scheduled ahead of the rotating gather
+    it overlaps)."""
     torch = _torch()
-    dev = torch.cuda.current_device()
-    if dev not in _SIDE:
-        _SIDE[dev] = torch.cuda.Stream(device=dev)
-    return _SIDE[dev]
+    key = (torch.cuda.current_device(), idx)
+    if key not in _SIDE:
+        _SIDE[key] = torch.cuda.Stream(device=key[0], priority=-1 if idx != 1 else 0)
+    return _SIDE[key]
 
 
 def _sm_count() -> int:
@@ -409,6 +424,19 @@ class PromptOut:
     scores: Optional["object"] = None  # fp32 [T] indexed by slab row (capture layer)
     logits: Optional["object"] = None  # fp32 [G, vocab] (last prompt row of each group)
     ml: Optional["object"] = None
+
+
+def segments_from_rows(rows: np.ndarray, deltas: np.ndarray) -> List[Tuple[int, int, int]]:
+    """Runs (row0, n, delta) of consecutive slab rows with one rotation delta
+    (context token i lives in slab row rows[i])."""
+    rows = np.asarray(rows, dtype=np.int64)
+    deltas = np.asarray(deltas, dtype=np.int64)
+    if rows.size == 0:
+        return []
+    cut = np.flatnonzero((np.diff(rows) != 1) | (np.diff(deltas) != 0)) + 1
+    starts = np.concatenate([[0], cut])
+    ends = np.concatenate([cut, [rows.size]])
+    return [(int(rows[a]), int(b - a), int(deltas[a])) for a, b in zip(starts, ends)]
 
 
 def segments_from_deltas(deltas: np.ndarray, row_offset: int = 0) -> List[Tuple[int, int, int]]:

@@ -363,3 +363,36 @@ def test_prefill_chunks_matches_oracle_per_chunk(cuda, precision, cfg_name):
     # the batched store feeds the path like separately prefilled chunks
     cache = P.assemble(got)
     assert cache.context_length == sum(lens)
+
+
+def test_store_path_fuses_rotation_into_assembly(cuda):
+    """Chunks from prefill_chunks take the fused path (scoring straight from
+    the store, one rotating gather into the decode layout): the selected set
+    and scores equal the two-pass path's bit for bit, the oracle's set, and the
+    recomputed cache equals the two-pass path's; the rotating gather equals
+    assemble + decode_view bit for bit."""
+    P = _pkg()
+    task = P.SyntheticTask(**C1_TASK)
+    dw, ow, g = _setup(P.c1_config(), 7, "bf16", task, 0)
+    kvs = P.prefill_chunks(dw, g.chunks)
+    assert all(c.store is kvs[0].store for c in kvs)
+    cfg = P.SelectionConfig(ratio=0.15)
+    fused = P.assemble_select_recompute(dw, kvs, g.chunks, g.prompt_token_ids, cfg)
+    plain_kvs = [P.ChunkKV(c.chunk_id, c.token_ids, c.keys.clone(), c.values.clone(), c.prefill_positions,
+                           c.provenance, c.model_fingerprint) for c in kvs]  # no store: the two-pass path
+    plain = P.assemble_select_recompute(dw, plain_kvs, g.chunks, g.prompt_token_ids, cfg)
+    np.testing.assert_array_equal(fused.selection.selected_numpy(), plain.selection.selected_numpy())
+    np.testing.assert_array_equal(fused.selection.scores_numpy(), plain.selection.scores_numpy())
+    oc = O.assemble([oracle_chunk(c) for c in kvs])
+    _, sel = O.run_selection(ow, oc, g.prompt_token_ids, ratio=0.15)
+    np.testing.assert_array_equal(fused.selection.selected_numpy(), sel)
+    import torch
+
+    assert torch.equal(fused.cache.keys, plain.cache.keys) and torch.equal(fused.cache.values, plain.cache.values)
+    np.testing.assert_array_equal(fused.cache.row_positions, plain.cache.row_positions)
+    from paper_2603_05353_b200.cache import assemble_decode_layout
+
+    rot = assemble_decode_layout(kvs, dw.config.rope_base)
+    want_k, _ = P.decode_view(P.assemble(kvs), dw.config.rope_base)
+    assert torch.equal(rot.keys, want_k[:, :rot.context_length])
+    np.testing.assert_array_equal(rot.row_positions, np.arange(rot.context_length))
