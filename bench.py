@@ -152,6 +152,9 @@ def dist_setup():
         # rank on the visible GPUs round-robin (a functional check of the
         # multi-process path on a one-GPU box); the default is NCCL, one GPU per rank.
         backend = os.environ.get("IFKV_DIST_BACKEND", "nccl")
+        if world > 1:  # communicator setup (ranks, channels, NVLS) visible in the driver's logs
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dev = local % max(1, torch.cuda.device_count())
         torch.cuda.set_device(dev)
         if backend == "nccl":

@@ -231,6 +231,8 @@ class Shard:
     chunk_ids: List[int]  # global declared-order indices of the owned chunks (ascending)
     global_rows: np.ndarray  # global context index of every local row (ascending)
     n_context: int
+    rank_rows: Optional[List[int]] = None  # context rows held by every rank (known to all ranks)
+    row_owner: Optional[np.ndarray] = None  # rank holding every global context row
 
 
 def make_shard(chunk_lengths: Sequence[int], rank: int, world: int, owners: Optional[np.ndarray] = None) -> Shard:
@@ -239,8 +241,9 @@ def make_shard(chunk_lengths: Sequence[int], rank: int, world: int, owners: Opti
     starts = np.concatenate([[0], np.cumsum(lens)[:-1]])
     mine = [int(c) for c in np.flatnonzero(owners == rank)]
     rows = [starts[c] + np.arange(lens[c]) for c in mine]
+    rank_rows = [int(lens[owners == r].sum()) for r in range(world)]
     return Shard(rank, world, mine, np.concatenate(rows).astype(np.int64) if rows else np.zeros(0, np.int64),
-                 int(lens.sum()))
+                 int(lens.sum()), rank_rows, np.repeat(owners, lens).astype(np.int64))
 
 
 # ---------------------------------------------------------------------------
@@ -354,7 +357,9 @@ def sharded_select(weights, shard: Shard, cache: AssembledCache, prompt_token_id
     grows = torch.as_tensor(shard.global_rows, device=scores.device)
     cand_idx = grows.index_select(0, loc)
     cand_s = scores.index_select(0, loc)
-    sel = merge_topk(comm.all_gather_var(cand_s), comm.all_gather_var(cand_idx), k)
+    # every rank's candidate count is known from the layout: no host round trip
+    sizes = [min(k, n) for n in shard.rank_rows] if shard.rank_rows is not None else None
+    sel = merge_topk(comm.all_gather_var(cand_s, sizes), comm.all_gather_var(cand_idx, sizes), k)
     return SelectionResult(scores=scores, selected=sel, strategy="attention-norm", geometry="GLOBAL")
 
 
@@ -380,8 +385,12 @@ def sharded_reorder(weights, chunks: Sequence, chunk_kvs: Sequence, shard: Shard
     else:
         imp_local = np.zeros(0, np.float64)
     dev = weights.device
-    ids = comm.all_gather_var(torch.as_tensor(np.asarray(shard.chunk_ids, np.int64), device=dev))
-    imps = comm.all_gather_var(torch.as_tensor(np.asarray(imp_local, np.float64), device=dev))
+    csizes = None
+    if shard.row_owner is not None:  # chunks per rank, known from the layout
+        starts0 = np.concatenate([[0], np.cumsum([c.local_length for c in chunks])[:-1]]).astype(np.int64)
+        csizes = np.bincount(shard.row_owner[starts0], minlength=shard.world).tolist()
+    ids = comm.all_gather_var(torch.as_tensor(np.asarray(shard.chunk_ids, np.int64), device=dev), csizes)
+    imps = comm.all_gather_var(torch.as_tensor(np.asarray(imp_local, np.float64), device=dev), csizes)
     importances = np.zeros(len(chunks), np.float64)
     for i, v in zip(ids, imps):
         importances[i.cpu().numpy()] = v.cpu().numpy()
@@ -393,8 +402,15 @@ def sharded_reorder(weights, chunks: Sequence, chunk_kvs: Sequence, shard: Shard
     order = sorted(range(len(shard.chunk_ids)), key=lambda i: slot_of[shard.chunk_ids[i]])
     owned = [shard.chunk_ids[i] for i in order]  # ascending in the permuted layout
     rows = [starts[slot_of[c]] + np.arange(lens[c]) for c in owned]
+    owners_perm = np.empty(int(n_total), np.int64)  # rank of every row in the permuted layout
+    all_owners = shard.row_owner
+    if all_owners is not None:
+        chunk_owner = np.array([all_owners[int(np.sum(lens[:c]))] for c in range(len(chunks))], np.int64)
+        for c in range(len(chunks)):
+            owners_perm[starts[slot_of[c]]: starts[slot_of[c]] + lens[c]] = chunk_owner[c]
     pshard = Shard(shard.rank, shard.world, owned,
-                   np.concatenate(rows).astype(np.int64) if rows else np.zeros(0, np.int64), int(n_total))
+                   np.concatenate(rows).astype(np.int64) if rows else np.zeros(0, np.int64), int(n_total),
+                   shard.rank_rows, owners_perm if all_owners is not None else None)
     local = assemble([chunk_kvs[i] for i in order])
     return permutation, importances, pshard, local
 
@@ -421,7 +437,12 @@ def sharded_recompute(weights, shard: Shard, cache: AssembledCache, selected_glo
     # per-rank query counts and the local causal horizons of every rank's
     # queries are layer-invariant: exchange them once, so the per-layer
     # collectives below need no host round trip (the GPU never drains)
-    hz_parts = comm.all_gather_var(sel_g)
+    if shard.row_owner is not None:  # per-rank query counts from the (replicated) selected set: one host sync
+        owner = torch.as_tensor(shard.row_owner, device=dev)
+        sizes = torch.bincount(owner.index_select(0, sel), minlength=comm.world).tolist()
+    else:
+        sizes = None
+    hz_parts = comm.all_gather_var(sel_g, sizes)
     sizes = [int(h.numel()) for h in hz_parts]
     hz_loc = [torch.searchsorted(grows, hp, right=True) - 1 for hp in hz_parts]  # local causal horizons
     hz_mine = hz_loc[comm.rank]

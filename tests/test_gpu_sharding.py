@@ -147,3 +147,103 @@ def test_sharded_reorder_matches_oracle(cuda, world):
     for _, _, pshard, lk in outs:
         got[:, pshard.global_rows] = lk[:, : pshard.global_rows.size]
     assert rel_err(got, want[:, :2048]) <= 1e-2
+
+
+# ---------------------------------------------------------------------------
+# real processes: TorchComm over torch.distributed with world size 2
+# ---------------------------------------------------------------------------
+
+
+def _two_proc_rank(rank, world, store_path, backend, q):
+    """One rank: the whole sharded path (select, recompute, reorder) at C1."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2603_05353_b200 as P
+    from paper_2603_05353_b200 import sharding as SH
+
+    dev = rank % torch.cuda.device_count()
+    torch.cuda.set_device(dev)
+    kw = {"device_id": torch.device("cuda", dev)} if backend == "nccl" else {}
+    dist.init_process_group(backend, init_method=f"file://{store_path}", rank=rank, world_size=world, **kw)
+    try:
+        cfg = P.c1_config()
+        dw = P.DeviceWeights.from_host(P.init_weights(cfg, 7), "bf16")
+        task = P.SyntheticTask(kind="uniform_noise", total_length=2048, fixed_size=256, prompt_length=32,
+                               vocab_size=1024)
+        g = P.generate_task(task, 1)
+        comm = SH.TorchComm()
+        shard = SH.make_shard([c.local_length for c in g.chunks], rank, world)
+        mine = [P.prefill_chunk(dw, g.chunks[i]) for i in shard.chunk_ids]
+        local = P.assemble(mine)
+        res = SH.sharded_select(dw, shard, local, g.prompt_token_ids, P.SelectionConfig(ratio=0.15), comm)
+        SH.sharded_recompute(dw, shard, local, res.selected, comm)
+        out = {"rows": shard.global_rows, "sel": res.selected.cpu().numpy(),
+               "scores": res.scores.double().cpu().numpy(), "k": local.keys.double().cpu().numpy(),
+               "v": local.values.double().cpu().numpy()}
+        perm, imps, pshard, plocal = SH.sharded_reorder(dw, g.chunks, mine, shard, g.prompt_token_ids, 308, comm)
+        res2 = SH.sharded_select(dw, pshard, plocal, g.prompt_token_ids, P.SelectionConfig(topk=308), comm)
+        out.update(perm=perm, imps=imps, sel2=res2.selected.cpu().numpy())
+        q.put((rank, out))
+    except Exception as exc:  # surfaced in the parent
+        import traceback
+
+        q.put((rank, RuntimeError(traceback.format_exc())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_process_torchcomm_path_matches_oracle(cuda):
+    """Two OS processes, TorchComm over torch.distributed (NCCL when two GPUs
+    are visible, else gloo with both ranks on the one GPU): sharded
+    selection, recompute and reorder at C1, every rank's selected set and the
+    reorder permutation bit-exact against the oracle, scores 1e-4, recomputed
+    K/V 1e-2."""
+    import os
+    import tempfile
+
+    import torch
+    import torch.multiprocessing as mp
+
+    import paper_2603_05353_b200 as P
+
+    world = 2
+    backend = "nccl" if torch.cuda.device_count() >= 2 else "gloo"
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    with tempfile.TemporaryDirectory() as tmp:
+        procs = [ctx.Process(target=_two_proc_rank, args=(r, world, os.path.join(tmp, "store"), backend, q))
+                 for r in range(world)]
+        for p in procs:
+            p.start()
+        outs = dict(q.get(timeout=300) for _ in range(world))
+        for p in procs:
+            p.join(timeout=60)
+    for v in outs.values():
+        if isinstance(v, Exception):
+            raise v
+    cfg = P.c1_config()
+    dw = P.DeviceWeights.from_host(P.init_weights(cfg, 7), "bf16")
+    ow = dw.to_host()
+    task = P.SyntheticTask(kind="uniform_noise", total_length=2048, fixed_size=256, prompt_length=32, vocab_size=1024)
+    g = P.generate_task(task, 1)
+    kvs = [P.prefill_chunk(dw, c) for c in g.chunks]
+    oc = O.assemble([oracle_chunk(c) for c in kvs])
+    scores, sel = O.run_selection(ow, oc, g.prompt_token_ids, ratio=0.15)
+    want = O.recompute_selected(ow, oc, *O.make_plan(oc.context_length, sel))
+    wk, wv = O.decode_view(want, cfg.rope_base)
+    perm, imps, _, _, sel2 = O.reorder_and_reselect(ow, [oracle_chunk(c) for c in kvs], g.prompt_token_ids, 308)
+    full = np.zeros(2048)
+    gk, gv = np.zeros_like(wk[:, :2048]), np.zeros_like(wv[:, :2048])
+    for r in range(world):
+        o = outs[r]
+        np.testing.assert_array_equal(o["sel"], sel)
+        np.testing.assert_array_equal(o["perm"], perm)
+        np.testing.assert_allclose(o["imps"], imps, rtol=1e-4)
+        np.testing.assert_array_equal(o["sel2"], sel2)
+        full[o["rows"]] = o["scores"]
+        gk[:, o["rows"]] = o["k"][:, :o["rows"].size]
+        gv[:, o["rows"]] = o["v"][:, :o["rows"].size]
+    np.testing.assert_allclose(full, scores, rtol=1e-4, atol=0)
+    assert rel_err(gk, wk[:, :2048]) <= 1e-2
+    assert rel_err(gv, wv[:, :2048]) <= 1e-2
