@@ -729,6 +729,74 @@ def cpu_sample(args, inp):
     return t_total, desc, threads
 
 
+REF_DIR = ROOT / "baseline" / "_ref"  # the reference package installed (pip --target), git-ignored
+
+
+def reference_c1_calibration(reps: int = 5):
+    """The REAL reference (chunkkv from baseline/_ref) on BASELINE config 1,
+    assemble + run_selection + make_plan + recompute_selected through its own
+    public API (harness.py:449-456), beside the oracle port on the same
+    inputs, in f32 and f64, on this host's cores: how fast the port used for
+    the C2 extrapolation is relative to the reference itself."""
+    import oracle as O
+
+    if not (REF_DIR / "chunkkv").exists():
+        return {"unavailable": f"{REF_DIR} not installed (pip install --target baseline/_ref)"}
+    sys.path.insert(0, str(REF_DIR))
+    try:
+        import chunkkv as ck
+    finally:
+        sys.path.remove(str(REF_DIR))
+    out = {"config": "C1: 2 layers, 4 heads x 128, d_ff 1792, 8 x 256 ctx + 32 prompt, r = 0.15 (k = 308)",
+           "reps": reps, "threads": _blas_threads()}
+    for prec in ("f32", "f64"):
+        cfg = ck.ModelConfig(n_layers=2, n_heads=4, d_model=512, d_head=128, d_ff=1792, vocab_size=1024,
+                             max_position=8192)
+        w = ck.init_weights(cfg, 7, precision=prec)
+        task = ck.SyntheticTask(kind="uniform_noise", total_length=2048, fixed_size=256, prompt_length=32,
+                                vocab_size=1024)
+        g = ck.generate_task(task, 0)
+        kvs = [ck.prefill_chunk(w, c) for c in g.chunks]
+        sel_cfg = ck.SelectionConfig(ratio=0.15)
+
+        def ref_step():
+            cache = ck.assemble(kvs)
+            res = ck.run_selection(w, g.chunks, cache, g.prompt_token_ids, sel_cfg)
+            ck.recompute_selected(w, cache, ck.make_plan(cache, res.selected))
+            return res.selected
+
+        ochunks = [O.Chunk(c.chunk_id, np.asarray(c.token_ids), np.stack(c.keys), np.stack(c.values),
+                           np.asarray(c.prefill_positions), 0) for c in kvs]
+
+        def port_step():
+            cache = O.assemble(ochunks)
+            _, sel = O.run_selection(w, cache, g.prompt_token_ids, ratio=0.15)
+            O.recompute_selected(w, cache, *O.make_plan(cache.context_length, sel))
+            return sel
+
+        tr, tp = [], []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            sel_r = ref_step()
+            tr.append(time.perf_counter() - t0)
+            t0 = time.perf_counter()
+            sel_p = port_step()
+            tp.append(time.perf_counter() - t0)
+        r_ms, p_ms = statistics.median(tr) * 1e3, statistics.median(tp) * 1e3
+        out[prec] = {"reference_ms": r_ms, "port_ms": p_ms, "port_over_reference_time": p_ms / r_ms,
+                     "same_selected_set": bool(np.array_equal(np.sort(np.asarray(sel_r)), sel_p))}
+    return out
+
+
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        return max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return None
@@ -744,8 +812,13 @@ def run_reference(args, world, rank):
     return {"metric": METRIC, "value": value, "unit": "ctx tok/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+            "extrapolated": True,
+            "extrapolation": "each step times a 2-layer Llama-width sample of the C2 workload on the host cores "
+                             "(~10-30 s) and extrapolates it to 32 layers / norm layer 19; ms_per_step is that "
+                             "extrapolated full-workload time, not the wall time of the step",
             "config": {"workload": "C2 sample (see cpu_baseline.sample)", "ctx_tokens": args.ctx},
             "cpu_baseline": {"value": value, "unit": "ctx tok/s", "cores": threads, "kind": "port", "sample": desc},
+            "reference_c1_calibration": reference_c1_calibration(),
             "e2e": {"value": value, "unit": "ctx tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -795,7 +868,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         t, desc, threads = cpu_sample(args, cpu_sample_setup(args))
         line["cpu_baseline"] = {"value": args.ctx / t, "unit": "ctx tok/s", "cores": threads, "kind": "port",
-                                "sample": desc}
+                                "sample": desc, "extrapolated": True,
+                                "reference_c1_calibration": reference_c1_calibration()}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
