@@ -46,7 +46,7 @@ METRIC = "assemble+select+recompute ms & ctx tok/s, Llama-3-8B shape, 32K ctx, 1
 
 # DRAM bytes per launch of the roofline kernels from one `ncu --set full`
 # capture (tools/gpu_prof.sh -> tools/ncu_traffic.py), committed under profiles/.
-TRAFFIC_FILE = ROOT / "profiles" / "r1_ncu_traffic.json"
+TRAFFIC_FILE = ROOT / "profiles" / "r2_ncu_traffic.json"
 
 
 def ncu_traffic(name):
@@ -341,11 +341,8 @@ def run_ours(args, world, rank, local):
     E.PROFILE = None
     attn = prof.get("recompute_attn", [])
     attn_ms = [a.elapsed_time(b) for a, b, _ in attn]
-    sct = [(a.elapsed_time(b), w) for a, b, w in prof.get("qkv_rope_scatter", [])]
     gem = [(a.elapsed_time(b), w) for a, b, w in prof.get("gemm", [])]
     pmm = [(a.elapsed_time(b), w) for a, b, w in prof.get("prompt_mm", [])]
-    rot = prof.get("rotate_rows", [])
-    rot_ms = [a.elapsed_time(b) for a, b, _ in rot]
     del res
 
     # timed region
@@ -402,25 +399,19 @@ def run_ours(args, world, rank, local):
             "peak_source": PEAKS["source"] + " sustained bf16",
             "algorithmic_flops_per_launch": flops_per_launch, "avg_launch_ms": attn_avg_ms,
             "launches_per_step": len(attn_ms), "share_of_step": float(np.sum(attn_ms)) / ms if attn_ms else None}
-    moved = float(rot[0][2]) if rot else 0.0  # rows whose rotation delta is nonzero (chunk 0 has delta 0)
-    rot_bytes = 2.0 * moved * L * cfg.kv_heads * Dh * 2  # read + write K of every moved row, all layers
+    # Kernel 1 (rotate_heads to global positions) runs inside the assemble
+    # gather (one read of every chunk row, one write of the decode-layout slab)
+    asm = [(a.elapsed_time(b), w) for a, b, w in prof.get("assemble_rotate", [])]
     rot_roof = None
-    if rot_ms:
-        ach = rot_bytes / (float(np.mean(rot_ms)) / 1e3) / 1e9
-        rot_roof = {"kernel": "ifkv rotate_rows (Kernel 1)", "bound": "hbm", "achieved": ach, "peak": PEAKS["hbm_gbs"],
-                    "unit": "GB/s", "frac": ach / PEAKS["hbm_gbs"], "frac_of_8tbs_spec": ach / HBM_SPEC_GBS,
-                    "avg_launch_ms": float(np.mean(rot_ms)),
-                    "algorithmic_bytes_per_launch": rot_bytes, "traffic": ncu_traffic("rotate_rows")}
-
-    sct_roof = None
-    if sct:  # fused rope + K/V scatter epilogue of the QKV GEMM (bytes per launch: qkv read, q/K/V written)
-        t_s, b_s = sum(t for t, _ in sct) / len(sct), sum(w for _, w in sct) / len(sct)
-        ach = b_s / (t_s / 1e3) / 1e9
-        sct_roof = {"kernel": "ifkv qkv_rope_scatter", "bound": "hbm", "achieved": ach, "peak": PEAKS["hbm_gbs"],
-                    "unit": "GB/s", "frac": ach / PEAKS["hbm_gbs"], "frac_of_8tbs_spec": ach / HBM_SPEC_GBS,
-                    "avg_launch_ms": t_s,
-                    "algorithmic_bytes_per_launch": b_s, "launches_per_step": len(sct),
-                    "traffic": ncu_traffic("qkv_rope_scatter")}
+    if asm:
+        t_a, b_a = sum(t for t, _ in asm) / len(asm), sum(w for _, w in asm) / len(asm)
+        ach = b_a / (t_a / 1e3) / 1e9
+        rot_roof = {"kernel": "ifkv assemble_gather_rotate (assemble + Kernel 1 fused)", "bound": "hbm",
+                    "achieved": ach, "peak": PEAKS["hbm_gbs"], "unit": "GB/s", "frac": ach / PEAKS["hbm_gbs"],
+                    "frac_of_8tbs_spec": ach / HBM_SPEC_GBS, "avg_launch_ms": t_a,
+                    "algorithmic_bytes_per_launch": b_a, "launches_per_step": len(asm),
+                    "traffic": ncu_traffic("assemble_gather")}
+    sct_roof = {"note": "the RoPE + in-place K/V scatter runs in the QKV GEMM epilogue (roofline_gemm)"}
 
     gemm_roof = None
     if gem:  # the tcgen05 projection GEMMs of the recompute (fused epilogues), all launches of one step

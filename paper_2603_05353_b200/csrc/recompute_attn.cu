@@ -117,7 +117,9 @@ extern "C" int ifkv_recompute_attn_tc_v5(const void* q, const void* k_layer, con
 // CTA, P staged in smem so S(j+1) follows the read of S(j); tiles of
 // floor(128/G) tokens x G heads; key splits below two waves.  Earlier
 // generations (v2: P in TMEM; v4: one tile per CTA, triple-buffered S) were
-// measured slower at every C2/C4 grid (profiles/r1_attn_ab.md) and removed.
+// measured slower at every C2/C4 grid (profiles/r1_attn_ab.md) and removed,
+// and so were the round-2 CTA-pair kernels v7-v9 (cta_group::2, P in TMEM;
+// 6-25 % slower than v5, profiles/r2_attn.md, sources in profiles/attic/).
 static int recompute_attn_tc_any(const void* q, const void* k_layer, const void* v_layer, const int64_t* horizon,
                                  int S, int H, int Hkv, int Dh, int n_rows, float scale, void* out, float* ml_out,
                                  void* stream, const int64_t* key_start = nullptr) {
