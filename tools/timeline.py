@@ -33,7 +33,7 @@ def main():
     cfg = bench.model_config(args)
     weights = P.DeviceWeights.random(cfg, seed=7, precision="bf16")
     gen = P.generate_task(bench.make_task(args, cfg), seed=0)
-    kvs = [P.prefill_chunk(weights, c) for c in gen.chunks]
+    kvs = P.prefill_chunks(weights, gen.chunks)  # one store slab, as bench.py prepares the context
     sel_cfg = P.SelectionConfig(ratio=args.ratio)
 
     def step():
@@ -78,6 +78,17 @@ def main():
     print("largest gaps (us, at ms, after -> before):")
     for g, a, b, at in gaps[:25]:
         print(f"  {g:9.1f} @ {at / 1e3:8.3f}  {str(a)[:50]} -> {str(b)[:50]}")
+    # the selection phase: from the first kernel to the first recompute GEMM
+    first_gemm = next((s for s, e, n in ks if "gemm_pair" in n), t1)
+    sel_k = [(s, e, n) for s, e, n in ks if s < first_gemm]
+    sel_busy = defaultdict(float)
+    for s, e, n in sel_k:
+        sel_busy[n.split("(")[0][-60:]] += (e - s)
+    sel_gap = sum(g for g, a, b, at in gaps if at + t0 < first_gemm)
+    print(f"selection phase: {(first_gemm - t0) / 1e3:.3f} ms to the first recompute GEMM, "
+          f"kernel time {sum(sel_busy.values()) / 1e3:.3f} ms, idle {sel_gap / 1e3:.3f} ms")
+    for n, d in sorted(sel_busy.items(), key=lambda x: -x[1])[:16]:
+        print(f"  {d / 1e3:8.3f}  {n}")
     # gap total per coarse phase (by position in the step)
     Path(args.out).parent.mkdir(parents=True, exist_ok=True)
     Path(args.out).write_text(json.dumps({"span_ms": span, "busy_ms": busy / 1e3,
