@@ -36,7 +36,7 @@ from .model import (
     qwen25vl_7b_config,
     toy_config,
 )
-from .pipeline import PathResult, StageTimer, assemble_select_recompute
+from .pipeline import PathResult, QueryGraph, StageTimer, assemble_select_recompute, query_graph
 from .positions import ChunkSpec, GeometryConfig, GeometryMode, PositionAssignment, assign_positions
 from .recompute import RecomputePlan, make_plan, recompute_selected
 from .reorder import ReorderPlan, reorder_and_reselect, score_chunks

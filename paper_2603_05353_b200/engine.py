@@ -80,6 +80,16 @@ def _s():
 # ---------------------------------------------------------------------------
 
 
+# CUDA-graph support (pipeline.QueryGraph): while H2D_CACHE is a dict, h2d
+# returns one device copy per distinct host content (the query's static
+# metadata: rows, work items, positions are uploaded once and the captured
+# graph reads them in place, with no host copy inside it); while CAPTURING, a
+# content that was not seen in the warm-up run is an error (a per-query host
+# input must reach a captured graph through a static device buffer).
+H2D_CACHE = None
+CAPTURING = False
+
+
 def h2d(a, device, dtype=None):
     """Host array -> device tensor through a pinned staging buffer with a
     non-blocking copy: the host never waits on the stream (pageable copies
@@ -87,9 +97,20 @@ def h2d(a, device, dtype=None):
     does not reuse the staging buffer before the copy has completed."""
     torch = _torch()
     arr = np.ascontiguousarray(a if dtype is None else np.asarray(a, dtype=dtype))
+    if H2D_CACHE is not None:
+        key = (arr.dtype.str, arr.shape, arr.tobytes(), str(device))
+        hit = H2D_CACHE.get(key)
+        if hit is not None:
+            return hit
+        if CAPTURING:
+            raise RuntimeError("host data that differs from the warm-up run reached a CUDA-graph capture")
     if arr.size == 0:
-        return torch.from_numpy(arr).to(device)
-    return torch.from_numpy(arr).pin_memory().to(device, non_blocking=True)
+        out = torch.from_numpy(arr).to(device)
+    else:
+        out = torch.from_numpy(arr).pin_memory().to(device, non_blocking=True)
+    if H2D_CACHE is not None:
+        H2D_CACHE[key] = out
+    return out
 
 
 def to_device_i64(a, device):
@@ -515,8 +536,9 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
     dev = weights.device
     H, Hkv, Dh, d = cfg.n_heads, cfg.kv_heads, cfg.d_head, cfg.d_model
     G = len(groups)
-    M = int(np.asarray(groups[0].token_ids).size)
-    if any(int(np.asarray(g.token_ids).size) != M for g in groups):
+    dev_ids = all(isinstance(g.token_ids, torch.Tensor) for g in groups)  # device prompt ids (graph replay)
+    M = int(groups[0].token_ids.numel() if dev_ids else np.asarray(groups[0].token_ids).size)
+    if any(int(g.token_ids.numel() if dev_ids else np.asarray(g.token_ids).size) != M for g in groups):
         raise ConfigurationError("all prompt groups must have the same length")
     bf16 = weights.precision == "bf16"
     mode = N.OUT_SPLIT3 if bf16 else N.OUT_F32
@@ -536,7 +558,10 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
     qsb_p = qc_p + 4 * qc_np.size
     qsl_p = qsb_p + 4 * qs_begin.size
     cs_delta = rope_table(np.asarray(deltas, np.int64) if deltas else np.zeros(1, np.int64), Dh, cfg.rope_base, dev)
-    ids = h2d(np.concatenate([np.asarray(g.token_ids, np.int64) for g in groups]), dev)
+    if dev_ids:
+        ids = torch.cat([g.token_ids.to(device=dev, dtype=torch.int64).reshape(-1) for g in groups])
+    else:
+        ids = h2d(np.concatenate([np.asarray(g.token_ids, np.int64) for g in groups]), dev)
     pos_all = np.concatenate([np.asarray(g.positions, np.int64) for g in groups])
     if pos_all.min() < 0 or pos_all.max() >= cfg.max_position:
         raise ConfigurationError(f"position outside [0, {cfg.max_position}): {int(pos_all.max())}")

@@ -103,8 +103,13 @@ def make_plan(cache: AssembledCache, selected) -> RecomputePlan:
     return RecomputePlan(selected=sel, positions=sel.copy(), allowed_upto=sel.copy())
 
 
-def recompute_selected(weights, cache: AssembledCache, plan: RecomputePlan) -> AssembledCache:
-    """Recompute the planned rows in place and return the updated cache."""
+def recompute_selected(weights, cache: AssembledCache, plan: RecomputePlan, readback=None) -> AssembledCache:
+    """Recompute the planned rows in place and return the updated cache.
+
+    ``readback`` (graph capture, pipeline.QueryGraph): two pinned int64 host
+    tensors of the plan's size; the selected indices and positions are copied
+    into them asynchronously and the host-side row metadata is left to the
+    caller (no host synchronisation here)."""
     torch = _torch()
     cfg = weights.config
     n = cache.context_length
@@ -124,8 +129,11 @@ def recompute_selected(weights, cache: AssembledCache, plan: RecomputePlan) -> A
     sel = E.to_device_i64(plan.selected, dev)
     pos = E.to_device_i64(plan.positions, dev)
     upto = E.to_device_i64(plan.allowed_upto, dev)
-    readback = None
-    if plan.trusted:  # device plan: start its copy to the host now, read it after the layer stack is queued
+    deferred = readback is not None
+    if deferred:
+        for h, t in zip(readback, (sel, pos)):
+            h.copy_(t, non_blocking=True)
+    elif plan.trusted:  # device plan: start its copy to the host now, read it after the layer stack is queued
         readback = [torch.empty(t.shape, dtype=torch.int64, pin_memory=True) for t in (sel, pos)]
         for h, t in zip(readback, (sel, pos)):
             h.copy_(t, non_blocking=True)
@@ -134,6 +142,8 @@ def recompute_selected(weights, cache: AssembledCache, plan: RecomputePlan) -> A
     to_decode_layout(cache, cfg.rope_base)
     ids = cache.token_ids_device().index_select(0, sel)
     E.layer_stack(weights, ids, pos, cache.keys, cache.values, sel, upto)
+    if deferred:
+        return cache
     # row metadata (host): positions and provenance of the replaced rows
     if readback is not None:
         done.synchronize()  # waits for the selection only, not for the recompute

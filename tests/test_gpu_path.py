@@ -396,3 +396,42 @@ def test_store_path_fuses_rotation_into_assembly(cuda):
     want_k, _ = P.decode_view(P.assemble(kvs), dw.config.rope_base)
     assert torch.equal(rot.keys, want_k[:, :rot.context_length])
     np.testing.assert_array_equal(rot.row_positions, np.arange(rot.context_length))
+
+
+@pytest.mark.parametrize("ratio", [0.15, 0.05])
+def test_query_graph_replays_match_eager(cuda, ratio):
+    """The CUDA-graph replay of a whole query (QueryGraph: ~450 launches as
+    one graph) returns the eager path's selected set, scores, recomputed slab
+    and row metadata bit for bit, for several prompts replayed through one
+    captured graph (the prompt ids reach it through a static device buffer);
+    the C1 selection also equals the oracle's.  ratio 0.05 exercises the
+    attention's key-split workspace (stream-ordered allocation inside the
+    graph)."""
+    import torch
+
+    P = _pkg()
+    task = P.SyntheticTask(**C1_TASK)
+    dw, ow, g = _setup(P.c1_config(), 7, "bf16", task, 0)
+    kvs = P.prefill_chunks(dw, g.chunks)
+    cfg = P.SelectionConfig(ratio=ratio)
+    rng = np.random.default_rng(5)
+    prompts = [np.asarray(g.prompt_token_ids)] + [rng.integers(0, 1024, 32) for _ in range(2)]
+    oc = O.assemble([oracle_chunk(c) for c in kvs])
+    for prompt in prompts + prompts[:1]:
+        eager = P.assemble_select_recompute(dw, kvs, g.chunks, prompt, cfg)
+        e_sel, e_sc = eager.selection.selected_numpy(), eager.selection.scores_numpy()
+        e_k, e_v, e_rp = eager.cache.keys.clone(), eager.cache.values.clone(), eager.cache.row_positions.copy()
+        del eager
+        got = P.assemble_select_recompute(dw, kvs, g.chunks, prompt, cfg, graph=True)
+        np.testing.assert_array_equal(got.selection.selected_numpy(), e_sel)
+        np.testing.assert_array_equal(got.selection.scores_numpy(), e_sc)
+        assert torch.equal(got.cache.keys, e_k) and torch.equal(got.cache.values, e_v)
+        np.testing.assert_array_equal(got.cache.row_positions, e_rp)
+        _, sel = O.run_selection(ow, oc, prompt, ratio=ratio)
+        np.testing.assert_array_equal(got.selection.selected_numpy(), sel)
+    qg = P.query_graph(dw, kvs, g.chunks, 32, cfg)
+    assert qg.launches > 50  # the whole query is in the graph
+    with pytest.raises(P.ConfigurationError):
+        qg.run(np.zeros(31, np.int64))
+    with pytest.raises(P.ConfigurationError):
+        qg.run(np.full(32, 5000, np.int64))
