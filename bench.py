@@ -407,7 +407,7 @@ def run_ours(args, world, rank, local):
             sc_host = res.selection.scores_numpy()
             torch.cuda.synchronize()
             times.append(time.perf_counter() - t0)
-            h2d = prompt.nbytes + res.cache.token_ids.nbytes
+            h2d = prompt.nbytes + (0 if use_graph else res.cache.token_ids.nbytes)  # graph: token ids are static
             d2h = sel_host.size * 8 + sc_host.size * 4
             del res
         e2e_ms = max_over_ranks(statistics.median(times) * 1e3, world)
