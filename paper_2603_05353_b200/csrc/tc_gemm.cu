@@ -169,10 +169,23 @@ __device__ __forceinline__ void qkv_chunk(const EpiParams& p, const float (&v)[3
   }
 }
 
+// Tile order: bands of `band` m-tiles, each band swept over every n-tile
+// (m fastest inside the band).  The pairs resident at once then share a few W
+// tiles and one band of A rows that fits L2: a large-M GEMM (the batched chunk
+// prefill, M = 32768) reads A once per band instead of once per n-tile.  With
+// band >= m_tiles this is the plain m-fastest order.
+__device__ __forceinline__ void tile_mn(int t, int m_tiles, int n_tiles, int band, int& mt, int& nt) {
+  const int per_band = band * n_tiles;
+  const int b = t / per_band, r = t - b * per_band;
+  const int bm = min(band, m_tiles - b * band);
+  nt = r / bm;
+  mt = b * band + (r - nt * bm);
+}
+
 template <int BM, int BN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<BM, BN>::kThreads, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_w,
-                     const __grid_constant__ CUtensorMap tm_out, int M, int N, int K, int m_tiles, int n_tiles,
+                     const __grid_constant__ CUtensorMap tm_out, int M, int N, int K, int m_tiles, int n_tiles, int band,
                      EpiParams p) {
   using C = Cfg<BM, BN>;
   constexpr int S = C::kStages;
@@ -216,8 +229,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<BM, BN>::kThread
       const uint32_t full0 = map_to_rank(full, 0);
       int it = 0;
       for (int t = pair; t < n_tile_total; t += n_pairs) {
-        const int m0 = (t % m_tiles) * BM + (int)rank * (BM / 2);
-        const int w0 = (t / m_tiles) * BN + (int)rank * (BN / 2);
+        int mt, nt;
+        tile_mn(t, m_tiles, n_tiles, band, mt, nt);
+        const int m0 = mt * BM + (int)rank * (BM / 2);
+        const int w0 = nt * BN + (int)rank * (BN / 2);
         for (int ks = 0; ks < k_steps; ++ks, ++it) {
           const int s = it % S;
           tc::mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
@@ -271,8 +286,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<BM, BN>::kThread
       const int buf = local % C::kBufs;
       tc::mbar_wait(&tfull[buf], (local / C::kBufs) & 1);
       tc::tc_fence_after();
-      const int row0 = (t % m_tiles) * BM + (int)rank * (BM / 2) + blk * 128 + ew * 32;  // this warp's rows
-      const int n0 = (t / m_tiles) * BN;
+      int mt, nt;
+      tile_mn(t, m_tiles, n_tiles, band, mt, nt);
+      const int row0 = mt * BM + (int)rank * (BM / 2) + blk * 128 + ew * 32;  // this warp's rows
+      const int n0 = nt * BN;
       const uint32_t tbase = tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)((buf + blk) * 256);
       if (EPI == EPI_SWIGLU) {
         // tile columns [128 b, 128 b + 64) gate, [128 b + 64, 128 b + 128) up
@@ -379,10 +396,13 @@ int launch_tile(const void* a, int64_t lda, int M, int K, const void* w, int N, 
     if (rc) return rc;
   }
   const int m_tiles = (M + BM - 1) / BM, n_tiles = (N + BN - 1) / BN;
+  // a band of A rows of <= ~40 MB (a third of L2) per n-tile sweep
+  const int64_t band_rows = (int64_t)40 * 1024 * 1024 / ((int64_t)K * 2);
+  const int band = (int)std::max<int64_t>(1, std::min<int64_t>(m_tiles, band_rows / BM));
   const int pairs = std::min(m_tiles * n_tiles, sm_count() / 2);
   auto kern = gemm_pair_kernel<BM, BN, EPI>;
   IFKV_CUDA_CALL(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem), "gemm: smem");
-  kern<<<2 * pairs, C::kThreads, C::kSmem, st>>>(ta, tw, to, M, N, K, m_tiles, n_tiles, p);
+  kern<<<2 * pairs, C::kThreads, C::kSmem, st>>>(ta, tw, to, M, N, K, m_tiles, n_tiles, band, p);
   IFKV_LAUNCH_CHECK("gemm");
   return IFKV_OK;
 }
