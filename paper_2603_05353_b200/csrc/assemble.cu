@@ -7,6 +7,8 @@
 // (model.py:254-270, as recompute.py:106-109 / decode_view cache.py:382-403
 // apply it) -- so the per-query slab comes out in the decode layout in ONE
 // pass over K instead of a gather followed by Kernel 1 in place.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace ifkv {
@@ -162,7 +164,10 @@ static int gather_launch(int dtype, int n_chunks, const void* const* src_k, cons
       if (w > max_work) max_work = w;
     }
     // enough CTAs per chunk that all chunks together fill ~8 CTAs per SM
-    int64_t per_chunk = ((int64_t)sms * 8 + nc - 1) / nc;
+    // (IFKV_GATHER_CPS: fewer, for a gather that runs beside other kernels)
+    int cps = 8;
+    if (const char* e = getenv("IFKV_GATHER_CPS")) cps = atoi(e) > 0 ? atoi(e) : 8;
+    int64_t per_chunk = ((int64_t)sms * cps + nc - 1) / nc;
     int64_t need = (max_work + 511) / 512;
     unsigned gx = (unsigned)(need < per_chunk ? (need > 0 ? need : 1) : per_chunk);
 #ifdef IFKV_GATHER_SHORT_CTAS

@@ -120,9 +120,18 @@ extern "C" int ifkv_recompute_attn_tc_v5(const void* q, const void* k_layer, con
 // measured slower at every C2/C4 grid (profiles/r1_attn_ab.md) and removed,
 // and so were the round-2 CTA-pair kernels v7-v9 (cta_group::2, P in TMEM;
 // 6-25 % slower than v5, profiles/r2_attn.md, sources in profiles/attic/).
+extern "C" int ifkv_recompute_attn_tc_v10(const void* q, const void* k_layer, const void* v_layer,
+                                          const int64_t* key_start, const int64_t* horizon, int S, int H, int Hkv,
+                                          int Dh, int n_rows, float scale, void* out, float* ml_out, void* stream);
+#ifndef IFKV_ATTN_GEN
+#define IFKV_ATTN_GEN 5
+#endif
 static int recompute_attn_tc_any(const void* q, const void* k_layer, const void* v_layer, const int64_t* horizon,
                                  int S, int H, int Hkv, int Dh, int n_rows, float scale, void* out, float* ml_out,
                                  void* stream, const int64_t* key_start = nullptr) {
+  if (IFKV_ATTN_GEN == 10)
+    return ifkv_recompute_attn_tc_v10(q, k_layer, v_layer, key_start, horizon, S, H, Hkv, Dh, n_rows, scale, out,
+                                      ml_out, stream);
   return ifkv_recompute_attn_tc_v5(q, k_layer, v_layer, key_start, horizon, S, H, Hkv, Dh, n_rows, scale, out,
                                    ml_out, stream);
 }

@@ -39,10 +39,13 @@ struct PSmem {
   uint32_t tmem_base;
 };
 
+// kMode is a template parameter so each mode gets its own register
+// allocation (one kernel for both modes needed 255 registers and spilled).
+template <int kMode>
 __global__ void __launch_bounds__(192, 1)
     prompt_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                           const __grid_constant__ CUtensorMap tm_v, const ifkv_attn_item* __restrict__ items, int H,
-                          int Hkv, int M, int hpt, int n_hchunks, int item_keys, float scale, int mode,
+                          int Hkv, int M, int hpt, int n_hchunks, int item_keys, float scale,
                           float* __restrict__ part_ml, float* __restrict__ part_o,
                           const float* __restrict__ ml_final, float* __restrict__ colsum) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -94,7 +97,7 @@ __global__ void __launch_bounds__(192, 1)
         tc::mbar_arrive_expect_tx(&sm.k_full[s], kTile);
         tc::tma_load_2d(sm.k[s], &tm_k, &sm.k_full[s], g * 128, row0);
         tc::tma_load_2d(sm.k[s] + kPanel, &tm_k, &sm.k_full[s], g * 128 + 64, row0);
-        if (mode == 0) {
+        if constexpr (kMode == 0) {
           tc::mbar_wait(&sm.v_empty[s], ph ^ 1);
           tc::mbar_arrive_expect_tx(&sm.v_full[s], kTile);
           tc::tma_load_2d(sm.v[s], &tm_v, &sm.v_full[s], g * 128, row0);
@@ -131,7 +134,7 @@ __global__ void __launch_bounds__(192, 1)
       issue_s(0);
       for (int j = 0; j < nblk; ++j) {
         if (j + 1 < nblk) issue_s(j + 1);
-        if (mode == 0) {
+        if constexpr (kMode == 0) {
           const int s = j & 1;
           tc::mbar_wait(&sm.p_full, j & 1);
           tc::mbar_wait(&sm.v_full[s], (j >> 1) & 1);
@@ -162,7 +165,7 @@ __global__ void __launch_bounds__(192, 1)
     // m_used: running max of the RAW scores; exponentials in log2 units
     const float sl2 = scale * 1.4426950408889634f;
     float m_used = -INFINITY, l = 0.f, mf2 = 0.f, inv_lf = 0.f;
-    if (mode == 1 && valid) {
+    if (kMode == 1 && valid) {
       const int64_t s = 2 * (((int64_t)it.group * H + h) * M + m);
       mf2 = ml_final[s] * 1.4426950408889634f;  // natural-unit max of the scaled logits -> log2 units
       inv_lf = 1.f / ml_final[s + 1];
@@ -183,7 +186,7 @@ __global__ void __launch_bounds__(192, 1)
         for (int c = 0; c < 128; ++c)
           if (c >= nk) v[c] = -INFINITY;
       }
-      if (mode == 0) {
+      if constexpr (kMode == 0) {
         // raw-score max (scale > 0 commutes with max), four FMNMX3 chains
         float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
@@ -216,6 +219,17 @@ __global__ void __launch_bounds__(192, 1)
         // P(j-1) consumed and O = PV(0..j-1) complete
         if (j > 0) tc::mbar_wait(&sm.pv_done, (j - 1) & 1);
         tc::tc_fence_after();
+        // P = hi + mid + lo (bf16 pairs), term t at TMEM cols kColP + 64 t + key / 2
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {  // 8-column stores keep the split terms' registers low (no spills)
+          uint32_t p0[8], p1[8], p2[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) tc::split3_pair(v[16 * q + 2 * u], v[16 * q + 2 * u + 1], p0[u], p1[u], p2[u]);
+          tc::tmem_st8(tmem + lane_off + kColP + 0 * 64 + 8 * q, p0);
+          tc::tmem_st8(tmem + lane_off + kColP + 1 * 64 + 8 * q, p1);
+          tc::tmem_st8(tmem + lane_off + kColP + 2 * 64 + 8 * q, p2);
+        }
+        // O rescale after the P terms are out of registers (v[] dead: no spills)
         if (j > 0 && __any_sync(0xffffffffu, need)) {
           const float a = need ? alpha : 1.f;
 #pragma unroll 1
@@ -227,16 +241,6 @@ __global__ void __launch_bounds__(192, 1)
             for (int u = 0; u < 16; ++u) o[u] *= a;
             tc::tmem_st16(tmem + lane_off + kColO + c * 16, reinterpret_cast<const uint32_t*>(o));
           }
-        }
-        // P = hi + mid + lo (bf16 pairs), term t at TMEM cols kColP + 64 t + key / 2
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint32_t p0[16], p1[16], p2[16];
-#pragma unroll
-          for (int u = 0; u < 16; ++u) tc::split3_pair(v[32 * q + 2 * u], v[32 * q + 2 * u + 1], p0[u], p1[u], p2[u]);
-          tc::tmem_st16(tmem + lane_off + kColP + 0 * 64 + 16 * q, p0);
-          tc::tmem_st16(tmem + lane_off + kColP + 1 * 64 + 16 * q, p1);
-          tc::tmem_st16(tmem + lane_off + kColP + 2 * 64 + 16 * q, p2);
         }
         l = l * alpha + sum;
         tc::tmem_st_wait();
@@ -256,7 +260,7 @@ __global__ void __launch_bounds__(192, 1)
           colsum[((int64_t)blockIdx.x * (Hkv * n_hchunks) + g * n_hchunks + hc) * item_keys + j * 128 + c] = acc;
       }
     }
-    if (mode == 0) {
+    if constexpr (kMode == 0) {
       tc::mbar_wait(&sm.pv_done, (nblk - 1) & 1);
       tc::tc_fence_after();
       const int64_t row_id = ((int64_t)blockIdx.x * H + h) * M + m;
@@ -333,12 +337,12 @@ static int launch_prompt_tc(int mode, const __nv_bfloat16* qd3, int n_qsets, con
     if (rc) return rc;
   }
   const size_t smem = sizeof(PSmem) + 1024;
-  IFKV_CUDA_CALL(cudaFuncSetAttribute(prompt_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+  auto kern = mode == 0 ? prompt_attn_tc_kernel<0> : prompt_attn_tc_kernel<1>;
+  IFKV_CUDA_CALL(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                  "prompt_attn_tc: smem attribute");
   dim3 grid(n_items, Hkv, n_hchunks);
-  prompt_attn_tc_kernel<<<grid, 192, smem, as_stream(stream)>>>(tq, tk, tv, items, H, Hkv, M, hpt, n_hchunks,
-                                                               item_keys, scale, mode, part_ml, part_o, ml_final,
-                                                               colsum);
+  kern<<<grid, 192, smem, as_stream(stream)>>>(tq, tk, tv, items, H, Hkv, M, hpt, n_hchunks, item_keys, scale, part_ml,
+                                               part_o, ml_final, colsum);
   IFKV_LAUNCH_CHECK("prompt_attn_tc");
   return IFKV_OK;
 }

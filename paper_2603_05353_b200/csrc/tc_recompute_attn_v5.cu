@@ -45,6 +45,11 @@ constexpr float kRescaleLog2 = 8.0f;
 #ifndef IFKV_ATTN5_SPLIT_MAX
 #define IFKV_ATTN5_SPLIT_MAX 4
 #endif
+// IFKV_ATTN5_SEQ (A/B): the exponential phases of the two tiles alternate
+// per SM sub-partition (A(j), B(j), A(j+1), ...) through per-warp mbarriers
+#ifndef IFKV_ATTN5_SEQ
+#define IFKV_ATTN5_SEQ 0
+#endif
 #ifndef IFKV_ATTN5_EXACTG
 #define IFKV_ATTN5_EXACTG 1
 #endif
@@ -55,6 +60,7 @@ struct Smem {
   uint8_t kv[kSlots][kTile];
   uint64_t q_full, full[kSlots], empty[kSlots];
   uint64_t s_full[2], s_free[2], p_full[2][2], pv_done[2][2], o_final[2];
+  uint64_t seq[2][4];
   uint32_t tmem_base;
   int n_blocks[2];
   int first_block;
@@ -97,7 +103,7 @@ __device__ __forceinline__ void st_p_chunk(uint8_t* p, int r, int panel, int c, 
   *reinterpret_cast<uint4*>(p + panel * kPanel + r * 128 + ((c ^ (r & 7)) << 4)) = v;
 }
 
-__device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int nblk, int b0, int t0, int S, int H,
+__device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int nblk, int ny, int b0, int t0, int S, int H,
                                              int G, int Gp, int g, const int64_t* __restrict__ horizon,
                                              const int64_t* __restrict__ key_start, float scale_log2,
                                              __nv_bfloat16* __restrict__ out, float* __restrict__ ml_out) {
@@ -232,6 +238,9 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
     }
     float sum = 0.f;
     const float2 sc2 = make_float2(scale_log2, scale_log2), mb2 = make_float2(-mb, -mb);
+#if IFKV_ATTN5_SEQ
+    if (x == 0 ? (j > 0 && j - 1 < ny) : (j < ny)) tc::mbar_wait(&sm.seq[x][w], (x == 0 ? j - 1 : j) & 1);
+#endif
 #pragma unroll
     for (int hf = 0; hf < 2; ++hf) {
       tc::tmem_ld32(t_s + hf * 64, v);
@@ -275,6 +284,9 @@ __device__ __forceinline__ void softmax_tile(Smem& sm, uint32_t tmem, int x, int
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&sm.p_full[x][hf]);
     }
+#if IFKV_ATTN5_SEQ
+    if (lane == 0 && (x == 0 ? j < ny : j + 1 < ny)) tc::mbar_arrive(&sm.seq[x ^ 1][w]);
+#endif
 #endif
     l = l * alpha + sum;
   }
@@ -352,6 +364,7 @@ __global__ void __launch_bounds__(384, 1)
       tc::mbar_init(&sm.pv_done[x][0], 1);
       tc::mbar_init(&sm.pv_done[x][1], 1);
       tc::mbar_init(&sm.o_final[x], 1);
+      for (int w = 0; w < 4; ++w) tc::mbar_init(&sm.seq[x][w], 1);
     }
     tc::fence_barrier_init();
   }
@@ -547,7 +560,9 @@ __global__ void __launch_bounds__(384, 1)
     const int x = (warp - 4) >> 2;
     const int nx = x == 0 ? nA : nB;
     const int tx = x == 0 ? tA : tB;
-    if (tx < S) softmax_tile(sm, tmem, x, nx, b0, tx, S, H, G, Gp, g, horizon, key_start, scale_log2, out, ml_out);
+    if (tx < S)
+      softmax_tile(sm, tmem, x, nx, x == 0 ? nB : nA, b0, tx, S, H, G, Gp, g, horizon, key_start, scale_log2, out,
+                   ml_out);
   }
   tc::tc_fence_before();
   __syncthreads();
