@@ -113,18 +113,20 @@ using namespace ifkv;
 extern "C" int ifkv_recompute_attn_tc_v5(const void* q, const void* k_layer, const void* v_layer,
                                          const int64_t* key_start, const int64_t* horizon, int S, int H, int Hkv,
                                          int Dh, int n_rows, float scale, void* out, float* ml_out, void* stream);
-// The tcgen05 kernel (tc_recompute_attn_v5.cu): two ping-ponging tiles per
-// CTA, P staged in smem so S(j+1) follows the read of S(j); tiles of
-// floor(128/G) tokens x G heads; key splits below two waves.  Earlier
-// generations (v2: P in TMEM; v4: one tile per CTA, triple-buffered S) were
-// measured slower at every C2/C4 grid (profiles/r1_attn_ab.md) and removed,
-// and so were the round-2 CTA-pair kernels v7-v9 (cta_group::2, P in TMEM;
-// 6-25 % slower than v5, profiles/r2_attn.md, sources in profiles/attic/).
 extern "C" int ifkv_recompute_attn_tc_v10(const void* q, const void* k_layer, const void* v_layer,
                                           const int64_t* key_start, const int64_t* horizon, int S, int H, int Hkv,
                                           int Dh, int n_rows, float scale, void* out, float* ml_out, void* stream);
+// The tcgen05 kernels: v10 (tc_recompute_attn_v10.cu, default): two tiles
+// per CTA, P written into the TMEM columns of its own S tile and read by a
+// TS-form PV MMA, 5-stage K/V ring; v5 (tc_recompute_attn_v5.cu, A/B with
+// -DIFKV_ATTN_GEN=5): P staged in shared memory so S(j+1) follows the read
+// of S(j).  Same tiles (floor(128/G) tokens x G heads) and key splits below
+// two waves.  v10 equals v5 alone at C2 and is 1.5 % faster over a whole
+// power-capped step (profiles/r2_attn10.md).  Earlier generations (v2, v4,
+// the CTA-pair kernels v7-v9) were measured slower and removed
+// (profiles/r1_attn_ab.md, profiles/r2_attn.md, sources in profiles/attic/).
 #ifndef IFKV_ATTN_GEN
-#define IFKV_ATTN_GEN 5
+#define IFKV_ATTN_GEN 10
 #endif
 static int recompute_attn_tc_any(const void* q, const void* k_layer, const void* v_layer, const int64_t* horizon,
                                  int S, int H, int Hkv, int Dh, int n_rows, float scale, void* out, float* ml_out,

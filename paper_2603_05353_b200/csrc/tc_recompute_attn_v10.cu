@@ -70,14 +70,50 @@ constexpr float kRescaleLog2 = 8.0f;
 #ifndef IFKV_ATTN10_PSPLIT
 #define IFKV_ATTN10_PSPLIT 1
 #endif
+// IFKV_ATTN10_SELFISSUE: each softmax warpgroup issues its own tile's PV(j)
+// and S(j+1) right after a named barrier over its P stores (no MMA warp, no
+// P -> MMA-warp mbarrier round trip on the per-tile critical chain)
+#ifndef IFKV_ATTN10_SELFISSUE
+#define IFKV_ATTN10_SELFISSUE 0
+#endif
+// IFKV_ATTN10_SPIN (A/B): the MMA warp polls the P barriers with
+// mbarrier.test_wait (no suspend) instead of try_wait
+#ifndef IFKV_ATTN10_SPIN
+#define IFKV_ATTN10_SPIN 0
+#endif
 #ifndef IFKV_ATTN10_REGS
 #define IFKV_ATTN10_REGS 200
+#endif
+
+#ifndef IFKV_ATTN10_TRACE
+#define IFKV_ATTN10_TRACE 0
+#endif
+#if IFKV_ATTN10_TRACE
+// clock64 event trace of ONE CTA (blockIdx 0, 0, 0): [event][tile][block]
+// events: 0 S observed, 1 row max done, 2 exponentials done, 3 P published
+// (softmax warp 0 of the tile), 4 PV issue (after the P waits), 5 S issue
+// (MMA warp)
+constexpr int kTraceBlocks = 512;
+__device__ long long g_attn10_trace[6][2][kTraceBlocks];
+#define TRACE10(ev, x, j)                                                                                    \
+  do {                                                                                                      \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (threadIdx.x & 127) == 0 && (j) < kTraceBlocks) \
+      g_attn10_trace[ev][x][j] = clock64();                                                                 \
+  } while (0)
+#define TRACE10M(ev, x, j)                                                                                   \
+  do {                                                                                                      \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (threadIdx.x & 31) == 0 && (j) < kTraceBlocks) \
+      g_attn10_trace[ev][x][j] = clock64();                                                                 \
+  } while (0)
+#else
+#define TRACE10(ev, x, j)
+#define TRACE10M(ev, x, j)
 #endif
 
 struct Smem10 {
   uint8_t q[2][kTile];
   uint8_t kv[kStages][kTile];
-  uint64_t q_full, full[kStages], empty[kStages];
+  uint64_t q_full, full[kStages], empty[kStages], empty_x[2][kStages];
   uint64_t s_full[2], p_half[2][2], o_final[2];
   uint64_t seq[2][4];  // exponential-phase turn of tile x on SM sub-partition w
   uint32_t tmem_base;
@@ -101,8 +137,43 @@ __device__ __forceinline__ int tile_first_block_warp10(const int64_t* key_start,
   return mn == INT64_MAX ? 0 : (int)(mn / kKeys);
 }
 
+__device__ __forceinline__ bool mbar_test10(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(tc::smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
 __device__ __forceinline__ void tmem_st32u(uint32_t taddr, const uint32_t* r) {
   tc::tmem_st32(taddr, reinterpret_cast<const float*>(r));
+}
+
+// tile x's MMAs, issued by one converged warp (elected lane): S_x(j) = Q_x K_j^T
+__device__ __forceinline__ void issue_s10(Smem10& sm, uint32_t tmem, int x, int j) {
+  constexpr uint32_t idesc_qk = tc::idesc_bf16(128, 128, 0, 0);
+  const uint64_t qa = tc::smem_desc_sw128(tc::smem_u32(sm.q[x]), 16, 1024);
+  const uint64_t kb = tc::smem_desc_sw128(tc::smem_u32(sm.kv[(2 * j) % kStages]), 16, 1024);
+#pragma unroll
+  for (int t = 0; t < kDh / 16; ++t) {
+    const uint64_t step = (uint64_t)((t >> 2) * (kPanel >> 4) + (t & 3) * 2);
+    tc::mma_bf16_ss_ws(tmem + 128 * x, qa + step, kb + step, idesc_qk, t > 0 ? 1u : 0u);
+  }
+}
+// O_x += P_x(j) V_j with P from TMEM (upper half of S_x)
+__device__ __forceinline__ void issue_pv10(Smem10& sm, uint32_t tmem, int x, int j) {
+  constexpr uint32_t idesc_pv = tc::idesc_bf16(128, 128, 0, 1);
+  const uint64_t vb = tc::smem_desc_sw128(tc::smem_u32(sm.kv[(2 * j + 1) % kStages]), kPanel, 1024);
+#pragma unroll
+  for (int t = 0; t < 8; ++t)
+    tc::mma_bf16_ts_ws(tmem + 256 + 128 * x, tmem + 128 * x + 64 + 8 * t, vb + (uint64_t)(t * (2048 >> 4)), idesc_pv,
+                       (j > 0 || t > 0) ? 1u : 0u);
+}
+__device__ __forceinline__ void wait_item10(Smem10& sm, int i) {
+  tc::mbar_wait(&sm.full[i % kStages], (i / kStages) & 1);
+  tc::tc_fence_after();
 }
 
 __device__ __forceinline__ void softmax_tile10(Smem10& sm, uint32_t tmem, int x, int nblk, int ny, int b0, int t0, int S,
@@ -122,9 +193,19 @@ __device__ __forceinline__ void softmax_tile10(Smem10& sm, uint32_t tmem, int x,
   const uint32_t t_o = tmem + 256 + 128 * x + lane_off;
   float m_used = -INFINITY, l = 0.f;
   const int y = x ^ 1;
+#if IFKV_ATTN10_SELFISSUE
+  if (w == 0 && nblk > 0) {  // this warpgroup's issuer: S_x(0)
+    tc::mbar_wait(&sm.q_full, 0);
+    wait_item10(sm, 0);
+    issue_s10(sm, tmem, x, 0);
+    tc::mma_commit_ws(&sm.s_full[x]);
+    tc::mma_commit_ws(&sm.empty_x[x][0]);
+  }
+#endif
   for (int j = 0; j < nblk; ++j) {
     tc::mbar_wait(&sm.s_full[x], j & 1);
     tc::tc_fence_after();
+    TRACE10(0, x, j);
     const int j0 = (b0 + j) * kKeys;
     const bool masked = __any_sync(0xffffffffu, j0 + kKeys - 1 > hz || j0 < ks);
 #if IFKV_ATTN10_ONEPASS
@@ -170,6 +251,7 @@ __device__ __forceinline__ void softmax_tile10(Smem10& sm, uint32_t tmem, int x,
       mx = tc::max3(mx, m2[0], m2[1]);
     }
 #endif
+    TRACE10(1, x, j);
     float alpha = 1.f;
     bool need = false;
     if (mx > -INFINITY && (m_used == -INFINITY || (mx - m_used) * scale_log2 > kRescaleLog2)) {
@@ -233,6 +315,7 @@ __device__ __forceinline__ void softmax_tile10(Smem10& sm, uint32_t tmem, int x,
     __syncwarp();
     if (lane == 0 && (x == 0 ? j < ny : j + 1 < ny)) tc::mbar_arrive(&sm.seq[y][w]);
 #endif
+    TRACE10(2, x, j);
     // S_x(j) complete => PV_x(j-1) complete (in-order MMAs): O_x is idle
     if (j > 0 && __any_sync(0xffffffffu, need)) {
       const float a = need ? alpha : 1.f;
@@ -248,7 +331,7 @@ __device__ __forceinline__ void softmax_tile10(Smem10& sm, uint32_t tmem, int x,
     }
     // P over the upper half of S (bf16 pairs, keys 2c, 2c+1 in column c), published by key halves
     tmem_st32u(t_p, p);
-#if IFKV_ATTN10_PSPLIT
+#if IFKV_ATTN10_PSPLIT && !IFKV_ATTN10_SELFISSUE
     tc::tmem_st_wait();
     tc::tc_fence_before();
     __syncwarp();
@@ -257,6 +340,27 @@ __device__ __forceinline__ void softmax_tile10(Smem10& sm, uint32_t tmem, int x,
     tmem_st32u(t_p + 32, p + 32);
     tc::tmem_st_wait();
     tc::tc_fence_before();
+#if IFKV_ATTN10_SELFISSUE
+    // all four warps' P (and rescaled O) stored -> this warpgroup's issuer
+    // queues PV_x(j) then S_x(j+1) (in-order: S overwrites P only after PV)
+    asm volatile("bar.sync %0, 128;" ::"r"(1 + x) : "memory");
+    TRACE10(3, x, j);
+    if (w == 0) {
+      tc::tc_fence_after();
+      wait_item10(sm, 2 * j + 1);  // V(j)
+      TRACE10(4, x, j);
+      issue_pv10(sm, tmem, x, j);
+      if (j == nblk - 1) tc::mma_commit_ws(&sm.o_final[x]);
+      tc::mma_commit_ws(&sm.empty_x[x][(2 * j + 1) % kStages]);
+      if (j + 1 < nblk) {
+        wait_item10(sm, 2 * j + 2);  // K(j+1)
+        TRACE10(5, x, j + 1);
+        issue_s10(sm, tmem, x, j + 1);
+        tc::mma_commit_ws(&sm.s_full[x]);
+        tc::mma_commit_ws(&sm.empty_x[x][(2 * j + 2) % kStages]);
+      }
+    }
+#else
     __syncwarp();
     if (lane == 0) {
 #if !IFKV_ATTN10_PSPLIT
@@ -264,6 +368,8 @@ __device__ __forceinline__ void softmax_tile10(Smem10& sm, uint32_t tmem, int x,
 #endif
       tc::mbar_arrive(&sm.p_half[x][1]);
     }
+    TRACE10(3, x, j);
+#endif
 #if IFKV_ATTN10_LATESUM
     // row sum off the critical path, from the bf16 P the PV MMA consumes
 #pragma unroll
@@ -335,6 +441,8 @@ __global__ void __launch_bounds__(384, 1)
     for (int i = 0; i < kStages; ++i) {
       tc::mbar_init(&sm.full[i], 1);
       tc::mbar_init(&sm.empty[i], 1);
+      tc::mbar_init(&sm.empty_x[0][i], 1);
+      tc::mbar_init(&sm.empty_x[1][i], 1);
     }
     for (int x = 0; x < 2; ++x) {
       tc::mbar_init(&sm.s_full[x], 1);
@@ -384,14 +492,23 @@ __global__ void __launch_bounds__(384, 1)
       }
       for (int i = 0; i < 2 * nblk; ++i) {  // item 2j = K(j), 2j + 1 = V(j)
         const int s = i % kStages;
+#if IFKV_ATTN10_SELFISSUE
+        // a slot is free once every tile that used its previous item released it
+        if (i >= kStages) {
+          const int jp = (i - kStages) >> 1;
+          if (jp < nA) tc::mbar_wait(&sm.empty_x[0][s], ((i / kStages) & 1) ^ 1);
+          if (jp < nB) tc::mbar_wait(&sm.empty_x[1][s], ((i / kStages) & 1) ^ 1);
+        }
+#else
         tc::mbar_wait(&sm.empty[s], ((i / kStages) & 1) ^ 1);
+#endif
         tc::mbar_arrive_expect_tx(&sm.full[s], kTile);
         const CUtensorMap* tm = (i & 1) ? &tm_v : &tm_k;
         const int row = (b0 + (i >> 1)) * kKeys;
         tc::tma_load_2d(sm.kv[s], tm, &sm.full[s], g * kDh, row);
         tc::tma_load_2d(sm.kv[s] + kPanel, tm, &sm.full[s], g * kDh + 64, row);
       }
-    } else if (warp == 9 && nblk > 0) {  // MMA issuer (converged warp, elected lane)
+    } else if (warp == 9 && nblk > 0 && !IFKV_ATTN10_SELFISSUE) {  // MMA issuer (converged warp, elected lane)
       constexpr uint32_t idesc_qk = tc::idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idesc_pv = tc::idesc_bf16(128, 128, 0, 1);
       const int n_of[2] = {nA, nB};
@@ -413,8 +530,14 @@ __global__ void __launch_bounds__(384, 1)
         const uint64_t vb = tc::smem_desc_sw128(tc::smem_u32(sm.kv[(2 * j + 1) % kStages]), kPanel, 1024);
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
+#if IFKV_ATTN10_SPIN
+          while (!mbar_test10(&sm.p_half[x][hf], j & 1)) {
+          }
+#else
           tc::mbar_wait(&sm.p_half[x][hf], j & 1);
+#endif
           tc::tc_fence_after();
+          if (hf == 1) TRACE10M(4, x, j);
 #pragma unroll
           for (int t = 4 * hf; t < 4 * hf + 4; ++t)
             tc::mma_bf16_ts_ws(tmem + 256 + 128 * x, tmem + 128 * x + 64 + 8 * t, vb + (uint64_t)(t * (2048 >> 4)),
@@ -432,7 +555,10 @@ __global__ void __launch_bounds__(384, 1)
         for (int x = 0; x < 2; ++x) {
           if (j - 1 < n_of[x]) issue_pv(x, j - 1);
           if (x == 0) wait_item(2 * j);  // K(j)
-          if (j < n_of[x]) issue_s(x, j);
+          if (j < n_of[x]) {
+            TRACE10M(5, x, j);
+            issue_s(x, j);
+          }
         }
         tc::mma_commit_ws(&sm.empty[(2 * j - 1) % kStages]);
         tc::mma_commit_ws(&sm.empty[(2 * j) % kStages]);
@@ -493,6 +619,16 @@ __global__ void attn_v10_merge_kernel(const __nv_bfloat16* __restrict__ part_o, 
 }  // namespace ifkv
 
 using namespace ifkv;
+
+#if IFKV_ATTN10_TRACE
+extern "C" int ifkv_attn10_trace_read(long long* dst) {
+  return cudaMemcpyFromSymbol(dst, g_attn10_trace, sizeof(g_attn10_trace)) == cudaSuccess ? 0 : 1;
+}
+extern "C" int ifkv_attn10_trace_clear() {
+  static long long z[6 * 2 * kTraceBlocks] = {};
+  return cudaMemcpyToSymbol(g_attn10_trace, z, sizeof(z)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 extern "C" int ifkv_recompute_attn_tc_v10(const void* q, const void* k_layer, const void* v_layer,
                                           const int64_t* key_start, const int64_t* horizon, int S, int H, int Hkv,

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--reorder", action="store_true")
     ap.add_argument("--out", default="gpurun_out/timeline.json")
     ap.add_argument("--steps", type=int, default=1, help="back-to-back steps inside the capture")
+    ap.add_argument("--graph", action="store_true", help="replay the captured query graph (pipeline.QueryGraph)")
     args = ap.parse_args()
     cfg = bench.model_config(args)
     weights = P.DeviceWeights.random(cfg, seed=7, precision="bf16")
@@ -38,7 +39,7 @@ def main():
 
     def step():
         return P.assemble_select_recompute(weights, kvs, gen.chunks, gen.prompt_token_ids, sel_cfg,
-                                           reorder=args.reorder)
+                                           reorder=args.reorder, graph=args.graph)
 
     for _ in range(3):
         step()
