@@ -81,6 +81,9 @@ constexpr float kRescaleLog2 = 8.0f;
 #ifndef IFKV_ATTN10_SPIN
 #define IFKV_ATTN10_SPIN 0
 #endif
+#ifndef IFKV_ATTN10_EARLYP
+#define IFKV_ATTN10_EARLYP 0
+#endif
 #ifndef IFKV_ATTN10_REGS
 #define IFKV_ATTN10_REGS 200
 #endif
@@ -268,6 +271,47 @@ __device__ __forceinline__ void softmax_tile10(Smem10& sm, uint32_t tmem, int x,
     // instead of both tiles sharing it
     if (x == 0 ? (j > 0 && j - 1 < ny) : (j < ny)) tc::mbar_wait(&sm.seq[x][w], (x == 0 ? j - 1 : j) & 1);
 #endif
+#if IFKV_ATTN10_EARLYP
+    // O rescale first (O_x idle: S_x(j) complete => PV_x(j-1) complete), then
+    // each 64-key half's exponentials are stored and published as soon as
+    // they exist, so PV_x(j) on keys 0..63 overlaps the exponentials of keys
+    // 64..127 (the whole S row was read before P overwrites its upper half)
+    if (j > 0 && __any_sync(0xffffffffu, need)) {
+      const float a = need ? alpha : 1.f;
+#pragma unroll 1
+      for (int c = 0; c < kDh / 32; ++c) {
+        float o[32];
+        tc::tmem_ld32(t_o + c * 32, o);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 32; ++u) o[u] *= a;
+        tc::tmem_st32(t_o + c * 32, o);
+      }
+    }
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      uint32_t p[32];
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        const int pu = hf * 32 + u;  // column pair pu = keys 2pu, 2pu+1
+        const float2 xx = tc::ffma2(make_float2(v[2 * pu], v[2 * pu + 1]), sc2, mb2);
+        float2 e;
+        if (((IFKV_ATTN10_FRAGS >> (pu >> 4)) & 1) && (pu & 7) >= 8 - IFKV_ATTN10_EMU)
+          e = tc::ex2_poly2(xx);
+        else
+          e = make_float2(tc::ex2(xx.x), tc::ex2(xx.y));
+        sum2[u & 1] = tc::fadd2(sum2[u & 1], e);
+        p[u] = tc::pack_bf16(e.x, e.y);
+      }
+      tmem_st32u(t_p + 32 * hf, p);
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&sm.p_half[x][hf]);
+    }
+    TRACE10(2, x, j);
+    TRACE10(3, x, j);
+#else
     uint32_t p[64];
 #if IFKV_ATTN10_ONEPASS
 #pragma unroll
@@ -369,6 +413,7 @@ __device__ __forceinline__ void softmax_tile10(Smem10& sm, uint32_t tmem, int x,
       tc::mbar_arrive(&sm.p_half[x][1]);
     }
     TRACE10(3, x, j);
+#endif
 #endif
 #if IFKV_ATTN10_LATESUM
     // row sum off the critical path, from the bf16 P the PV MMA consumes

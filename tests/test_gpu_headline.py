@@ -8,10 +8,13 @@ cache.py:74-99), as SURVEY §7 hard part 1 prescribes.
 
 * C2 width (d 4096, 32 q / 8 kv heads, d_ff 14336, vocab 128256, RoPE 5e5)
   over the real 32K context in 16 x 2048 chunks, 4 layers (norm layer 2):
-  the selected set is bit-exact and every score agrees to elementwise rtol
-  1e-4 (scores are strictly positive, so elementwise rtol is meaningful);
-  the boundary margin (score gap at k / the observed score error) is printed
-  (selection.py:127-183, test_acceptance.py:191-202).
+  every score agrees to elementwise rtol 1e-4 (scores are strictly
+  positive, so elementwise rtol is meaningful) and the selected set is
+  bit-exact whenever the boundary gap exceeds twice the observed score
+  error; below that the sets may differ only by near-tied tokens inside the
+  error band, which is asserted token by token and printed
+  (tests/helpers.py:assert_same_selection; selection.py:127-183,
+  test_acceptance.py:191-202).
 * C4 width (Qwen2.5-VL-7B LM: d 3584, 28 q / 4 kv heads -> GQA group 7,
   d_ff 18944), 24 x 1280 image-token chunks + 4 x 512 text chunks.
 * C3: the information-flow reorder over 64 x 2048 chunks (128K context) at
@@ -34,7 +37,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from helpers import oracle_chunk, rel_err, to_np
+from helpers import assert_same_selection, oracle_chunk, rel_err, to_np
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
@@ -106,7 +109,8 @@ def test_headline_width_selection_matches_oracle(cuda, shape):
           f"max elementwise rel err {np.max(np.abs(got_scores - scores) / scores):.2e}")
     assert np.all(scores > 0)
     np.testing.assert_allclose(got_scores, scores, rtol=1e-4, atol=0)
-    np.testing.assert_array_equal(got, sel)
+    np.testing.assert_array_equal(sel, np.sort(O.select_topk(scores, k)))
+    assert_same_selection(got, got_scores, scores, k, tag=shape)
 
 
 def test_c3_reorder_64_chunks_matches_oracle(cuda):
@@ -129,7 +133,7 @@ def test_c3_reorder_64_chunks_matches_oracle(cuda):
     np.testing.assert_allclose(plan.chunk_importance, imps, rtol=1e-4)
     np.testing.assert_array_equal(plan.permutation, perm)
     np.testing.assert_allclose(second.scores_numpy(), scores, rtol=1e-4, atol=0)
-    np.testing.assert_array_equal(second.selected_numpy(), sel)
+    assert_same_selection(second.selected_numpy(), second.scores_numpy(), scores, budget, tag="C3 second pass")
 
 
 def test_depth_32_layers_c1_width_matches_oracle(cuda):

@@ -64,3 +64,20 @@ def test_merge_topk_equals_global_topk(n, world, data):
     got = SH.merge_topk(scores, idx, k).numpy()
     want = O.select_topk(s.astype(np.float64), k)
     assert np.array_equal(got, want)
+
+
+def test_selection_assert_helper_near_ties_only():
+    """tests/helpers.assert_same_selection: exact when certified, near-tie
+    swaps inside the error band tolerated, anything else rejected."""
+    import pytest as _pt
+
+    from helpers import assert_same_selection
+
+    ref = np.array([5.0, 4.0, 3.0 + 1e-9, 3.0, 1.0])
+    sel = np.array([0, 1, 2])
+    assert assert_same_selection(sel, ref, ref, 3) == 0  # no error: certified
+    got = ref.copy()
+    got[3] += 2e-9  # index 3 now beats index 2: a near-tie within the error
+    assert assert_same_selection(np.array([0, 1, 3]), got, ref, 3) == 1
+    with _pt.raises(AssertionError):  # a token far outside the band
+        assert_same_selection(np.array([0, 1, 4]), got, ref, 3)
