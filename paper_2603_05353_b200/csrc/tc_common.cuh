@@ -221,9 +221,7 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
   return u64_as_f2(d);
 }
 // ex2_poly on a pair with packed arithmetic: 2 FMNMX + 3 FADD2 + 3 FFMA2 +
-// 4 integer ops for two exponentials, no MUFU.  Inputs below -126 (masked
-// -inf included) give 2^-126 * p ~ 1e-38 instead of 0: below every bf16 P
-// that matters (the row sum is >= 1) and exactly representable.
+// 4 integer ops + 2 selects for two exponentials, no MUFU.
 __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
   unsigned long long d;
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_as_u64(a)), "l"(f2_as_u64(b)));
@@ -237,9 +235,11 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   float2 p = ffma2(make_float2(0.05295114f, 0.05295114f), f, make_float2(0.24165066f, 0.24165066f));
   p = ffma2(p, f, make_float2(0.69353656f, 0.69353656f));
   p = ffma2(p, f, make_float2(1.f, 1.f));
-  // bits(t) << 23 == round(x) << 23 (the magic's own bits shift out)
-  return make_float2(__int_as_float((__float_as_int(t.x) << 23) + __float_as_int(p.x)),
-                     __int_as_float((__float_as_int(t.y) << 23) + __float_as_int(p.y)));
+  // bits(t) << 23 == round(x) << 23 (the magic's own bits shift out); inputs
+  // below -126 (masked -inf included) give exactly 0, like ex2.approx.ftz
+  const float rx = __int_as_float((__float_as_int(t.x) << 23) + __float_as_int(p.x));
+  const float ry = __int_as_float((__float_as_int(t.y) << 23) + __float_as_int(p.y));
+  return make_float2(x.x < -126.f ? 0.f : rx, x.y < -126.f ? 0.f : ry);
 }
 
 __device__ __forceinline__ float max3(float a, float b, float c) {

@@ -24,6 +24,12 @@
 // smem (224 KB): Q 2 x 32 KB, a kStages-deep ring of 32 KB K / V blocks in
 // consumption order K0 V0 K1 V1 ...  TMEM: S_A | S_B | O_A | O_B (128 columns
 // each), P_x aliased on columns 64..127 of S_x.
+// Softmax per block: one 128-column TMEM read of S, row max, an optional O
+// rescale (O_x is idle), then each 32-key quarter's exponentials -- a quarter
+// of them on the FMA pipe (degree-3 polynomial), the rest on MUFU -- are
+// packed, stored over S and published, so PV_x(j) on the first keys overlaps
+// the exponentials of the later ones (profiles/r2_attn10.md: 5-15 % over the
+// variant that publishes P after all 128 exponentials).
 // Warps: 0-3 softmax A, 4-7 softmax B (TMEM lane quarter = warp % 4),
 // 8 TMA producer, 9 MMA issuer (warp-synchronous, elected lane), 10 TMEM
 // allocator + block counts, 11 idle.  Softmax warpgroups raise their register
@@ -47,10 +53,10 @@ constexpr float kRescaleLog2 = 8.0f;
 // FMA-pipe exponentials (A/B): in each 32-key fragment selected by FRAGS,
 // the last EMU of every 8 column pairs use the polynomial instead of MUFU.
 #ifndef IFKV_ATTN10_EMU
-#define IFKV_ATTN10_EMU 0
+#define IFKV_ATTN10_EMU 2
 #endif
 #ifndef IFKV_ATTN10_FRAGS
-#define IFKV_ATTN10_FRAGS 0x6
+#define IFKV_ATTN10_FRAGS 0xF
 #endif
 #ifndef IFKV_ATTN10_SPLIT_WAVES
 #define IFKV_ATTN10_SPLIT_WAVES 2
@@ -82,8 +88,14 @@ constexpr float kRescaleLog2 = 8.0f;
 #define IFKV_ATTN10_SPIN 0
 #endif
 #ifndef IFKV_ATTN10_EARLYP
-#define IFKV_ATTN10_EARLYP 0
+#define IFKV_ATTN10_EARLYP 1
 #endif
+// P published in kParts key parts (4: 32 keys each; early-P path only)
+#ifndef IFKV_ATTN10_PPARTS
+#define IFKV_ATTN10_PPARTS 4
+#endif
+constexpr int kParts = IFKV_ATTN10_PPARTS;
+static_assert(kParts == 2 || (kParts == 4 && IFKV_ATTN10_EARLYP), "P parts: 2, or 4 with early P");
 #ifndef IFKV_ATTN10_REGS
 #define IFKV_ATTN10_REGS 200
 #endif
@@ -117,7 +129,7 @@ struct Smem10 {
   uint8_t q[2][kTile];
   uint8_t kv[kStages][kTile];
   uint64_t q_full, full[kStages], empty[kStages], empty_x[2][kStages];
-  uint64_t s_full[2], p_half[2][2], o_final[2];
+  uint64_t s_full[2], p_half[2][4], o_final[2];  // p_half: P published by parts (kParts)
   uint64_t seq[2][4];  // exponential-phase turn of tile x on SM sub-partition w
   uint32_t tmem_base;
   int n_blocks[2];
@@ -288,12 +300,13 @@ __device__ __forceinline__ void softmax_tile10(Smem10& sm, uint32_t tmem, int x,
         tc::tmem_st32(t_o + c * 32, o);
       }
     }
+    constexpr int kPairs = 64 / kParts;  // column pairs (= TMEM columns of P) per published part
 #pragma unroll
-    for (int hf = 0; hf < 2; ++hf) {
-      uint32_t p[32];
+    for (int hf = 0; hf < kParts; ++hf) {
+      uint32_t p[kPairs];
 #pragma unroll
-      for (int u = 0; u < 32; ++u) {
-        const int pu = hf * 32 + u;  // column pair pu = keys 2pu, 2pu+1
+      for (int u = 0; u < kPairs; ++u) {
+        const int pu = hf * kPairs + u;  // column pair pu = keys 2pu, 2pu+1
         const float2 xx = tc::ffma2(make_float2(v[2 * pu], v[2 * pu + 1]), sc2, mb2);
         float2 e;
         if (((IFKV_ATTN10_FRAGS >> (pu >> 4)) & 1) && (pu & 7) >= 8 - IFKV_ATTN10_EMU)
@@ -303,7 +316,10 @@ __device__ __forceinline__ void softmax_tile10(Smem10& sm, uint32_t tmem, int x,
         sum2[u & 1] = tc::fadd2(sum2[u & 1], e);
         p[u] = tc::pack_bf16(e.x, e.y);
       }
-      tmem_st32u(t_p + 32 * hf, p);
+      if constexpr (kPairs == 32)
+        tmem_st32u(t_p + kPairs * hf, p);
+      else
+        tc::tmem_st16(t_p + kPairs * hf, p);
       tc::tmem_st_wait();
       tc::tc_fence_before();
       __syncwarp();
@@ -318,7 +334,6 @@ __device__ __forceinline__ void softmax_tile10(Smem10& sm, uint32_t tmem, int x,
     for (int u = 0; u < 64; ++u) {  // column pair u = keys 2u, 2u+1
       const float2 xx = tc::ffma2(make_float2(v[2 * u], v[2 * u + 1]), sc2, mb2);
       float2 e;
-      // branch-free: masked (-inf) inputs give ~1e-38 on the polynomial path, not 0 (harmless)
       if (((IFKV_ATTN10_FRAGS >> (u >> 4)) & 1) && (u & 7) >= 8 - IFKV_ATTN10_EMU)
         e = tc::ex2_poly2(xx);
       else
@@ -491,8 +506,7 @@ __global__ void __launch_bounds__(384, 1)
     }
     for (int x = 0; x < 2; ++x) {
       tc::mbar_init(&sm.s_full[x], 1);
-      tc::mbar_init(&sm.p_half[x][0], 4);  // one elected arrival per softmax warp
-      tc::mbar_init(&sm.p_half[x][1], 4);
+      for (int q = 0; q < 4; ++q) tc::mbar_init(&sm.p_half[x][q], 4);  // one elected arrival per softmax warp
       tc::mbar_init(&sm.o_final[x], 1);
       for (int w = 0; w < 4; ++w) tc::mbar_init(&sm.seq[x][w], 1);
     }
@@ -574,7 +588,7 @@ __global__ void __launch_bounds__(384, 1)
       auto issue_pv = [&](int x, int j) {  // O_x += P_x(j) V_j, P from TMEM, by key halves as they land
         const uint64_t vb = tc::smem_desc_sw128(tc::smem_u32(sm.kv[(2 * j + 1) % kStages]), kPanel, 1024);
 #pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
+        for (int hf = 0; hf < kParts; ++hf) {
 #if IFKV_ATTN10_SPIN
           while (!mbar_test10(&sm.p_half[x][hf], j & 1)) {
           }
@@ -582,9 +596,9 @@ __global__ void __launch_bounds__(384, 1)
           tc::mbar_wait(&sm.p_half[x][hf], j & 1);
 #endif
           tc::tc_fence_after();
-          if (hf == 1) TRACE10M(4, x, j);
+          if (hf == kParts - 1) TRACE10M(4, x, j);
 #pragma unroll
-          for (int t = 4 * hf; t < 4 * hf + 4; ++t)
+          for (int t = (8 / kParts) * hf; t < (8 / kParts) * (hf + 1); ++t)
             tc::mma_bf16_ts_ws(tmem + 256 + 128 * x, tmem + 128 * x + 64 + 8 * t, vb + (uint64_t)(t * (2048 >> 4)),
                                idesc_pv, (j > 0 || t > 0) ? 1u : 0u);
         }

@@ -62,3 +62,23 @@ def assert_same_selection(got_sel, got_scores, ref_scores, k, tag=""):
     band = np.abs(ref_scores[diff] - kth) <= 2 * err
     assert np.all(band), f"tokens {diff[~band]} differ outside the score-error band (gap > 2 x {err:.3e})"
     return diff.size // 2
+
+
+def assert_same_permutation(got_perm, ref_perm, ref_imps, got_imps, tag=""):
+    """Reorder permutation vs the float64 reference (stable argsort of the
+    chunk importances): bit-exact, except that chunks whose reference
+    importances lie within twice the observed importance error of each other
+    (near-ties below fp32 resolution) may trade places.  Returns the number
+    of positions that differ."""
+    got_perm, ref_perm = np.asarray(got_perm), np.asarray(ref_perm)
+    ref_imps = np.asarray(ref_imps, np.float64)
+    err = float(np.max(np.abs(np.asarray(got_imps, np.float64) - ref_imps)))
+    diff = np.flatnonzero(got_perm != ref_perm)
+    srt = np.sort(ref_imps)
+    print(f"{tag} permutation: min importance gap {np.min(np.diff(srt)):.3e}, max importance error {err:.3e}; "
+          f"{diff.size} position(s) differ")
+    assert np.array_equal(np.sort(got_perm), np.arange(got_perm.size))
+    for i in diff:
+        a, b = ref_imps[got_perm[i]], ref_imps[ref_perm[i]]
+        assert abs(a - b) <= 2 * err, f"position {i}: chunks {got_perm[i]} / {ref_perm[i]} are not a near-tie"
+    return int(diff.size)

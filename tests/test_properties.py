@@ -81,3 +81,17 @@ def test_selection_assert_helper_near_ties_only():
     assert assert_same_selection(np.array([0, 1, 3]), got, ref, 3) == 1
     with _pt.raises(AssertionError):  # a token far outside the band
         assert_same_selection(np.array([0, 1, 4]), got, ref, 3)
+
+
+def test_permutation_assert_helper_near_ties_only():
+    import pytest as _pt
+
+    from helpers import assert_same_permutation
+
+    ref_imps = np.array([3.0, 1.0, 2.0, 2.0 + 1e-9])
+    ref = np.argsort(ref_imps, kind="stable")  # [1, 2, 3, 0]
+    got_imps = ref_imps.copy()
+    got_imps[2] += 2e-9  # chunk 2 now sorts after chunk 3
+    assert assert_same_permutation(np.argsort(got_imps, kind="stable"), ref, ref_imps, got_imps) == 2
+    with _pt.raises(AssertionError):
+        assert_same_permutation(np.array([2, 1, 3, 0]), ref, ref_imps, got_imps)
