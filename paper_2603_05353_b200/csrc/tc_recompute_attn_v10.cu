@@ -44,8 +44,11 @@ constexpr int kKeys = 128;
 constexpr int kDh = 128;
 constexpr int kPanel = 128 * 128;  // 128 rows x 128 B (64 bf16)
 constexpr int kTile = 2 * kPanel;  // 32 KB
+#ifndef IFKV_ATTN10_WIDE
+#define IFKV_ATTN10_WIDE 0
+#endif
 #ifndef IFKV_ATTN10_STAGES
-#define IFKV_ATTN10_STAGES 5
+#define IFKV_ATTN10_STAGES (IFKV_ATTN10_WIDE ? 4 : 5)  // wide: 6 KB of row-max exchange buffers
 #endif
 constexpr int kStages = IFKV_ATTN10_STAGES;
 constexpr uint32_t kTmemCols = 512;
@@ -96,6 +99,18 @@ constexpr float kRescaleLog2 = 8.0f;
 #endif
 constexpr int kParts = IFKV_ATTN10_PPARTS;
 static_assert(kParts == 2 || (kParts == 4 && IFKV_ATTN10_EARLYP), "P parts: 2, or 4 with early P");
+// IFKV_ATTN10_WIDE: two softmax warps per TMEM lane quarter and tile, each
+// owning 64 of the 128 keys of a block (row max exchanged through shared
+// memory): the other half of a row's softmax work runs in parallel
+#if IFKV_ATTN10_WIDE
+constexpr uint32_t kPCol0 = 0, kPColGap = 32;  // P of keys 0..63 at S columns 0..31, keys 64..127 at 64..95
+constexpr int kThreads = 640;  // warps 0-15 softmax (tile = (w >> 2) & 1, half = w >> 3), 16 TMA, 17 MMA, 18 TMEM
+constexpr int kWarpTma = 16, kWarpMma = 17, kWarpAlloc = 18;
+#else
+constexpr uint32_t kPCol0 = 64, kPColGap = 0;  // P over the upper half of S
+constexpr int kThreads = 384;
+constexpr int kWarpTma = 8, kWarpMma = 9, kWarpAlloc = 10;
+#endif
 #ifndef IFKV_ATTN10_REGS
 #define IFKV_ATTN10_REGS 200
 #endif
@@ -131,6 +146,10 @@ struct Smem10 {
   uint64_t q_full, full[kStages], empty[kStages], empty_x[2][kStages];
   uint64_t s_full[2], p_half[2][4], o_final[2];  // p_half: P published by parts (kParts)
   uint64_t seq[2][4];  // exponential-phase turn of tile x on SM sub-partition w
+#if IFKV_ATTN10_WIDE
+  float xmax[2][2][2][128];  // [block parity][tile][key half][row]: row max exchange
+  float xl[2][2][128];       // [tile][key half][row]: row sums at the end
+#endif
   uint32_t tmem_base;
   int n_blocks[2];
   int first_block;
@@ -472,7 +491,150 @@ __device__ __forceinline__ void softmax_tile10(Smem10& sm, uint32_t tmem, int x,
   }
 }
 
-__global__ void __launch_bounds__(384, 1)
+#if IFKV_ATTN10_WIDE
+// Two warps per lane quarter and tile: warp half h owns keys 64h..64h+63 of
+// every block, P columns 64 + 32h.., O columns 64h..  (bar.sync id 1 + 4x + w
+// pairs the two warps of a row quarter).
+__device__ __forceinline__ void softmax_tile10w(Smem10& sm, uint32_t tmem, int x, int hh, int nblk, int b0, int t0,
+                                                int S, int H, int G, int g, const int64_t* __restrict__ horizon,
+                                                const int64_t* __restrict__ key_start, float scale_log2,
+                                                __nv_bfloat16* __restrict__ out, float* __restrict__ ml_out) {
+  const int w = (threadIdx.x >> 5) & 3;
+  const int lane = threadIdx.x & 31;
+  const int row = w * 32 + lane;
+  const int tok = t0 + row / G;
+  const bool valid = row < (kRows / G) * G && tok < S;
+  const int hz = valid ? (int)horizon[tok] : INT_MAX;
+  const int ks = valid && key_start ? (int)key_start[tok] : 0;
+  const uint32_t lane_off = (uint32_t)(w * 32) << 16;
+  const uint32_t t_s = tmem + 128 * x + lane_off + 64 * hh;
+  // P of this warp's 64 keys goes into its OWN (already read) S columns:
+  // keys 64hh..64hh+63 -> columns 64hh..64hh+31, so no warp overwrites S the
+  // other warp of the row has not read yet
+  const uint32_t t_p = tmem + 128 * x + lane_off + 64 * hh;
+  const uint32_t t_o = tmem + 256 + 128 * x + lane_off + 64 * hh;
+  const int bar = 1 + 4 * x + w;
+  float m_used = -INFINITY, l = 0.f;
+  for (int j = 0; j < nblk; ++j) {
+    tc::mbar_wait(&sm.s_full[x], j & 1);
+    tc::tc_fence_after();
+    const int j0 = (b0 + j) * kKeys + 64 * hh;
+    const bool masked = __any_sync(0xffffffffu, j0 + 63 > hz || j0 < ks);
+    // pass 1: this warp's row max over its 64 keys, 32 columns at a time
+    float v[32];
+    float m2[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      tc::tmem_ld32(t_s + 32 * q, v);
+      tc::tmem_ld_wait();
+      if (masked) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          if (j0 + 32 * q + c > hz || j0 + 32 * q + c < ks) v[c] = -INFINITY;
+      }
+#pragma unroll
+      for (int c = 0; c < 32; c += 4) {
+        m2[0] = tc::max3(m2[0], v[c], v[c + 1]);
+        m2[1] = tc::max3(m2[1], v[c + 2], v[c + 3]);
+      }
+    }
+    sm.xmax[j & 1][x][hh][row] = fmaxf(m2[0], m2[1]);
+    asm volatile("bar.sync %0, 64;" ::"r"(bar) : "memory");
+    const float mx = fmaxf(sm.xmax[j & 1][x][0][row], sm.xmax[j & 1][x][1][row]);
+    float alpha = 1.f;
+    bool need = false;
+    if (mx > -INFINITY && (m_used == -INFINITY || (mx - m_used) * scale_log2 > kRescaleLog2)) {
+      need = true;
+      alpha = m_used == -INFINITY ? 0.f : tc::ex2((m_used - mx) * scale_log2);
+      m_used = mx;
+    }
+    const float mb = m_used == -INFINITY ? 0.f : m_used * scale_log2;
+    const float2 sc2 = make_float2(scale_log2, scale_log2), mb2 = make_float2(-mb, -mb);
+    if (j > 0 && __any_sync(0xffffffffu, need)) {  // O_x idle; this warp rescales its 64 O columns
+      const float a = need ? alpha : 1.f;
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        float o[32];
+        tc::tmem_ld32(t_o + c * 32, o);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 32; ++u) o[u] *= a;
+        tc::tmem_st32(t_o + c * 32, o);
+      }
+    }
+    float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    // pass 2: per 32 keys, re-read S, exponentiate, store P over the S
+    // columns just read (own region), publish
+#pragma unroll
+    for (int part = 0; part < 2; ++part) {
+      tc::tmem_ld32(t_s + 32 * part, v);
+      tc::tmem_ld_wait();
+      if (masked) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          if (j0 + 32 * part + c > hz || j0 + 32 * part + c < ks) v[c] = -INFINITY;
+      }
+      uint32_t p[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int pu = 32 * hh + part * 16 + u;  // pair within the block (emulation pattern)
+        const float2 xx = tc::ffma2(make_float2(v[2 * u], v[2 * u + 1]), sc2, mb2);
+        float2 e;
+        if (((IFKV_ATTN10_FRAGS >> (pu >> 4)) & 1) && (pu & 7) >= 8 - IFKV_ATTN10_EMU)
+          e = tc::ex2_poly2(xx);
+        else
+          e = make_float2(tc::ex2(xx.x), tc::ex2(xx.y));
+        sum2[u & 1] = tc::fadd2(sum2[u & 1], e);
+        p[u] = tc::pack_bf16(e.x, e.y);
+      }
+      tc::tmem_st16(t_p + 16 * part, p);
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&sm.p_half[x][2 * hh + part]);
+    }
+    l = l * alpha + ((sum2[0].x + sum2[1].x) + (sum2[0].y + sum2[1].y));
+  }
+  if (nblk > 0) {
+    tc::mbar_wait(&sm.o_final[x], 0);
+    tc::tc_fence_after();
+  }
+  sm.xl[x][hh][row] = l;
+  asm volatile("bar.sync %0, 64;" ::"r"(bar) : "memory");
+  const float lt = sm.xl[x][0][row] + sm.xl[x][1][row];
+  const float inv = lt > 0.f ? 1.f / lt : 0.f;
+  const int64_t orow = (int64_t)tok * H + g * G + row % G;
+  __nv_bfloat16* dst = out + orow * kDh + 64 * hh;
+  if (ml_out && valid && hh == 0) {
+    ml_out[2 * orow] = m_used == -INFINITY ? -INFINITY : m_used * scale_log2 * 0.6931471805599453f;
+    ml_out[2 * orow + 1] = lt;
+  }
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    float o[32];
+    if (nblk > 0) {
+      tc::tmem_ld32(t_o + c * 32, o);
+      tc::tmem_ld_wait();
+    } else {
+#pragma unroll
+      for (int u = 0; u < 32; ++u) o[u] = 0.f;
+    }
+    if (valid) {
+#pragma unroll
+      for (int u = 0; u < 32; u += 8) {
+        uint4 pk;
+        pk.x = tc::pack_bf16(o[u] * inv, o[u + 1] * inv);
+        pk.y = tc::pack_bf16(o[u + 2] * inv, o[u + 3] * inv);
+        pk.z = tc::pack_bf16(o[u + 4] * inv, o[u + 5] * inv);
+        pk.w = tc::pack_bf16(o[u + 6] * inv, o[u + 7] * inv);
+        *reinterpret_cast<uint4*>(dst + c * 32 + u) = pk;
+      }
+    }
+  }
+}
+#endif
+
+__global__ void __launch_bounds__(kThreads, 1)
     recompute_attn_v10_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                               const __grid_constant__ CUtensorMap tm_v, const int64_t* __restrict__ horizon,
                               const int64_t* __restrict__ key_start, int S, int H, int Hkv, float scale_log2,
@@ -485,7 +647,7 @@ __global__ void __launch_bounds__(384, 1)
   const int g = blockIdx.x;
   const int pair = gridDim.y - 1 - blockIdx.y;  // heaviest (latest) pairs first
   const int tA = pair * 2 * tok, tB = tA + tok;
-  if (warp == 10) {
+  if (warp == kWarpAlloc) {
     const int a = tA < S ? tile_blocks_warp10(horizon, tA, tok, S) : 0;
     const int b = tB < S ? tile_blocks_warp10(horizon, tB, tok, S) : 0;
     const int fa = tA < S ? tile_first_block_warp10(key_start, tA, tok, S) : INT_MAX;
@@ -522,7 +684,7 @@ __global__ void __launch_bounds__(384, 1)
     }
     tc::fence_async_smem();
   }
-  if (warp == 10) tc::tmem_alloc<kTmemCols>(&sm.tmem_base);
+  if (warp == kWarpAlloc) tc::tmem_alloc<kTmemCols>(&sm.tmem_base);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -536,9 +698,11 @@ __global__ void __launch_bounds__(384, 1)
   out += (int64_t)blockIdx.z * S * H * kDh;
   if (ml_out) ml_out += (int64_t)blockIdx.z * S * H * 2;
 
-  if (warp >= 8) {
+  if (warp >= kWarpTma) {
+#if !IFKV_ATTN10_WIDE  // (wide: every warp keeps the 96 registers of a 640-thread launch)
     tc::reg_dealloc<96>();  // setmaxnreg moves registers within the CTA: 256 x (200 - 168) <= 128 x (168 - 96)
-    if (warp == 8 && lane == 0 && nblk > 0) {  // TMA producer
+#endif
+    if (warp == kWarpTma && lane == 0 && nblk > 0) {  // TMA producer
       tc::tma_prefetch(&tm_q);
       tc::tma_prefetch(&tm_k);
       tc::tma_prefetch(&tm_v);
@@ -567,7 +731,7 @@ __global__ void __launch_bounds__(384, 1)
         tc::tma_load_2d(sm.kv[s], tm, &sm.full[s], g * kDh, row);
         tc::tma_load_2d(sm.kv[s] + kPanel, tm, &sm.full[s], g * kDh + 64, row);
       }
-    } else if (warp == 9 && nblk > 0 && !IFKV_ATTN10_SELFISSUE) {  // MMA issuer (converged warp, elected lane)
+    } else if (warp == kWarpMma && nblk > 0 && !IFKV_ATTN10_SELFISSUE) {  // MMA issuer (converged warp, elected lane)
       constexpr uint32_t idesc_qk = tc::idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idesc_pv = tc::idesc_bf16(128, 128, 0, 1);
       const int n_of[2] = {nA, nB};
@@ -599,8 +763,8 @@ __global__ void __launch_bounds__(384, 1)
           if (hf == kParts - 1) TRACE10M(4, x, j);
 #pragma unroll
           for (int t = (8 / kParts) * hf; t < (8 / kParts) * (hf + 1); ++t)
-            tc::mma_bf16_ts_ws(tmem + 256 + 128 * x, tmem + 128 * x + 64 + 8 * t, vb + (uint64_t)(t * (2048 >> 4)),
-                               idesc_pv, (j > 0 || t > 0) ? 1u : 0u);
+            tc::mma_bf16_ts_ws(tmem + 256 + 128 * x, tmem + 128 * x + kPCol0 + 8 * t + (t >= 4 ? kPColGap : 0),
+                               vb + (uint64_t)(t * (2048 >> 4)), idesc_pv, (j > 0 || t > 0) ? 1u : 0u);
         }
         if (j == n_of[x] - 1) tc::mma_commit_ws(&sm.o_final[x]);
       };
@@ -628,6 +792,12 @@ __global__ void __launch_bounds__(384, 1)
       tc::mma_commit_ws(&sm.empty[(2 * nblk - 1) % kStages]);
     }
   } else {
+#if IFKV_ATTN10_WIDE
+    const int x = (warp >> 2) & 1, hh = warp >> 3;
+    const int nx = x == 0 ? nA : nB;
+    const int tx = x == 0 ? tA : tB;
+    if (tx < S) softmax_tile10w(sm, tmem, x, hh, nx, b0, tx, S, H, G, g, horizon, key_start, scale_log2, out, ml_out);
+#else
     tc::reg_alloc<IFKV_ATTN10_REGS>();
     const int x = warp >> 2;
     const int nx = x == 0 ? nA : nB;
@@ -635,10 +805,11 @@ __global__ void __launch_bounds__(384, 1)
     if (tx < S)
       softmax_tile10(sm, tmem, x, nx, x == 0 ? nB : nA, b0, tx, S, H, G, g, horizon, key_start, scale_log2, out,
                      ml_out);
+#endif
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 10) tc::tmem_dealloc<kTmemCols>(tmem);
+  if (warp == kWarpAlloc) tc::tmem_dealloc<kTmemCols>(tmem);
 }
 
 // Key-split partials -> output, fixed split order (as v5's merge).
@@ -728,7 +899,7 @@ extern "C" int ifkv_recompute_attn_tc_v10(const void* q, const void* k_layer, co
   if (Hkv * pairs < IFKV_ATTN10_SPLIT_WAVES * sms)
     P = min(IFKV_ATTN10_SPLIT_MAX, (IFKV_ATTN10_SPLIT_WAVES * sms + Hkv * pairs - 1) / (Hkv * pairs));
   if (P == 1) {
-    recompute_attn_v10_kernel<<<dim3(Hkv, pairs, 1), 384, smem, st>>>(tq, tk, tv, horizon, key_start, S, H, Hkv,
+    recompute_attn_v10_kernel<<<dim3(Hkv, pairs, 1), kThreads, smem, st>>>(tq, tk, tv, horizon, key_start, S, H, Hkv,
                                                                       scale_log2, (__nv_bfloat16*)out, ml_out);
     IFKV_LAUNCH_CHECK("recompute_attn_v10");
     return IFKV_OK;
@@ -742,7 +913,7 @@ extern "C" int ifkv_recompute_attn_tc_v10(const void* q, const void* k_layer, co
   }
   auto* part_o = reinterpret_cast<__nv_bfloat16*>(ws);
   auto* part_ml = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + o_bytes);
-  recompute_attn_v10_kernel<<<dim3(Hkv, pairs, P), 384, smem, st>>>(tq, tk, tv, horizon, key_start, S, H, Hkv,
+  recompute_attn_v10_kernel<<<dim3(Hkv, pairs, P), kThreads, smem, st>>>(tq, tk, tv, horizon, key_start, S, H, Hkv,
                                                                     scale_log2, part_o, part_ml);
   IFKV_LAUNCH_CHECK("recompute_attn_v10 (split)");
   attn_v10_merge_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(part_o, part_ml, P, rows, (__nv_bfloat16*)out,
