@@ -188,10 +188,12 @@ int ifkv_score_columns(int kv_dtype, const float* qd, const void* k_slab, const 
  * q, k rotated by cs[row]; kp, vp fp32 [G*M][Hkv][Dh]; for every query set s
  * of the row's group g (qs_list[qs_begin[g] .. qs_begin[g+1])) qd[s][h][m] =
  * R(-cs_delta[qset_cs[s]]) q (qset_cs < 0: no rotation), qd3 (optional) its
- * bf16 hi/mid/lo terms [n_qsets][3][H][M][Dh]. */
+ * bf16 hi/mid/lo terms [n_qsets][3][H][M][Dh]; with qd3 given, qd is written
+ * only for the unrotated sets (the SIMT prompt items' input).  n_qsets: the
+ * total number of query sets (bounds every group's count). */
 int ifkv_prompt_qkv(const float* qkv, int n_parts, int G, int M, int H, int Hkv, int Dh, const float* cs,
-                    const int32_t* qs_begin, const int32_t* qs_list, const int32_t* qset_cs, const float* cs_delta,
-                    float* kp, float* vp, float* qd, void* qd3, void* stream);
+                    const int32_t* qs_begin, const int32_t* qs_list, const int32_t* qset_cs, int n_qsets,
+                    const float* cs_delta, float* kp, float* vp, float* qd, void* qd3, void* stream);
 /* Rotated query sets: qd[s] = R(-cs[qset_cs[s]]) q[qset_group[s]], transposed
  * from q [G][M][H][Dh] to [H][M][Dh]; qset_cs[s] < 0 means no rotation.
  * qd3 (optional, bf16 [n_qsets][3][H][M][Dh]) receives the hi/mid/lo split

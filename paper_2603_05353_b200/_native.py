@@ -53,7 +53,7 @@ SIGNATURES = {
     "ifkv_recompute_attn_partial": [I32, P, P, P, P, I32, I32, I32, I32, I32, F32, P, P, P],
     "ifkv_merge_partials": [P, P, I32, I64, I32, P, P, P],
     "ifkv_merge_prompt_states": [P, P, I32, I32, I32, I32, I32, P, P, P],
-    "ifkv_prompt_qkv": [P, I32, I32, I32, I32, I32, I32, P, P, P, P, P, P, P, P, P, P],
+    "ifkv_prompt_qkv": [P, I32, I32, I32, I32, I32, I32, P, P, P, P, I32, P, P, P, P, P, P],
     "ifkv_gemm": [P, I64, I32, I32, P, I32, I32, P, I64, I32, I32, P],
     "ifkv_gemm_qkv_rope_scatter": [P, I64, I32, I32, P, I32, I32, I32, P, P, P, P, P, I32, P],
     "ifkv_gemm_swiglu": [P, I64, I32, I32, P, I32, P, I32, P],

@@ -168,6 +168,7 @@ __global__ void rotate_queries_kernel(const float* __restrict__ q, int M, int H,
 // each of its group's query sets (q . R(d) k == (R(-d) q) . k, the context
 // keys stay as stored) into qd [s][H][M][Dh] (+ the bf16 split terms qd3).
 // Group g's query sets: qs_list[qs_begin[g] .. qs_begin[g+1]).
+constexpr int kQsetsPerThread = 4;
 __global__ void prompt_qkv_kernel(const float* __restrict__ qkv, int n_parts, int64_t part_stride, int G, int M,
                                   int H, int Hkv, int Dh, const float2* __restrict__ cs,
                                   const int32_t* __restrict__ qs_begin, const int32_t* __restrict__ qs_list,
@@ -194,6 +195,7 @@ __global__ void prompt_qkv_kernel(const float* __restrict__ qkv, int n_parts, in
     x1 = y1;
   }
   if (head >= H) {
+    if (blockIdx.y != 0) return;
     float* d = (head < H + Hkv ? kp + ((int64_t)r * Hkv + (head - H)) * Dh
                                : vp + ((int64_t)r * Hkv + (head - H - Hkv)) * Dh) + 2 * pi;
     d[0] = x0;
@@ -202,7 +204,10 @@ __global__ void prompt_qkv_kernel(const float* __restrict__ qkv, int n_parts, in
   }
   const int g = r / M, m = r % M;
   const int64_t plane = (int64_t)H * M * Dh;
-  for (int k = qs_begin[g]; k < qs_begin[g + 1]; ++k) {
+  // blockIdx.y: this thread's slab of kQsetsPerThread of the group's query sets
+  const int k0 = qs_begin[g] + blockIdx.y * kQsetsPerThread;
+  const int k1 = min(qs_begin[g + 1], k0 + kQsetsPerThread);
+  for (int k = k0; k < k1; ++k) {
     const int s = qs_list[k], ci = qset_cs[s];
     float y0 = x0, y1 = x1;
     if (ci >= 0) {
@@ -211,8 +216,10 @@ __global__ void prompt_qkv_kernel(const float* __restrict__ qkv, int n_parts, in
       y1 = -x0 * a.y + x1 * a.x;
     }
     const int64_t o = (((int64_t)s * H + head) * M + m) * Dh + 2 * pi;
-    qd[o] = y0;
-    qd[o + 1] = y1;
+    if (!qd3 || ci < 0) {  // fp32 sets: the SIMT kernels' input (tensor-core path: only the prompt's own, delta 0)
+      qd[o] = y0;
+      qd[o + 1] = y1;
+    }
     if (qd3) {  // [n_qsets][3][H][M][Dh]
       const int64_t o3 = ((int64_t)s * 3) * plane + (o - (int64_t)s * plane);
       __nv_bfloat16 a0, a1, a2, b0, b1, b2;
@@ -529,13 +536,17 @@ extern "C" int ifkv_rotate_queries(const float* q, int G, int M, int H, int Dh, 
 }
 
 extern "C" int ifkv_prompt_qkv(const float* qkv, int n_parts, int G, int M, int H, int Hkv, int Dh, const float* cs,
-                               const int32_t* qs_begin, const int32_t* qs_list, const int32_t* qset_cs,
+                               const int32_t* qs_begin, const int32_t* qs_list, const int32_t* qset_cs, int n_qsets,
                                const float* cs_delta, float* kp, float* vp, float* qd, void* qd3, void* stream) {
   IFKV_CHECK_ARG(Dh % 2 == 0 && Hkv > 0 && H > 0 && H % Hkv == 0 && n_parts >= 1 && G > 0 && M > 0,
                  "prompt_qkv: bad shape");
+  IFKV_CHECK_ARG(n_qsets >= 1, "prompt_qkv: n_qsets must be >= 1");
   const int64_t total = (int64_t)G * M * (H + 2 * Hkv) * (Dh / 2);
   const int64_t part_stride = (int64_t)G * M * (H + 2 * Hkv) * Dh;
-  prompt_qkv_kernel<<<(unsigned)((total + 255) / 256), 256, 0, as_stream(stream)>>>(
+  // grid.y: slabs of kQsetsPerThread query sets (n_qsets bounds every group's
+  // count; slabs past a group's end return at once)
+  const dim3 grid((unsigned)((total + 255) / 256), (unsigned)((n_qsets + kQsetsPerThread - 1) / kQsetsPerThread));
+  prompt_qkv_kernel<<<grid, 256, 0, as_stream(stream)>>>(
       qkv, n_parts, part_stride, G, M, H, Hkv, Dh, reinterpret_cast<const float2*>(cs), qs_begin, qs_list, qset_cs,
       reinterpret_cast<const float2*>(cs_delta), kp, vp, qd, reinterpret_cast<__nv_bfloat16*>(qd3));
   IFKV_LAUNCH_CHECK("prompt_qkv");

@@ -590,7 +590,7 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
         x = add_rmsnorm(h, pending, pending_parts, lw.attn_norm, mode)
         qkv = mm_parts(x, lw.wqkv)
         N.call("ifkv_prompt_qkv", N.ptr(qkv), qkv.shape[0], G, M, H, Hkv, Dh, N.ptr(cs_prompt), qsb_p, qsl_p, qc_p,
-               N.ptr(cs_delta), N.ptr(kp), N.ptr(vp), N.ptr(qd), N.ptr(qd3), _s())
+               n_qsets, N.ptr(cs_delta), N.ptr(kp), N.ptr(vp), N.ptr(qd), N.ptr(qd3), _s())
         capture = capture_layer is not None and li == capture_layer
         with _Bracket("prompt_attn", li):
             side = include_prompt and use_tc and n_ctx and torch.cuda.is_available()
