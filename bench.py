@@ -100,15 +100,32 @@ def parse():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and clock-event (throttle) reasons sampled every 20 ms during
+    the timed region through NVML (nvidia-ml-py), falling back to
+    `nvidia-smi -lms 200` when NVML is unavailable."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    BITS = [0x8, 0x40, 0x20, 0x4]  # nvmlClocksEventReason{HwSlowdown,HwThermalSlowdown,SwThermalSlowdown,SwPowerCap}
 
     def __init__(self, index: int):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.proc, self.nvml = index, [], None, None
+        self.stop_evt = threading.Event()
 
     def start(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.nvml = (pynvml, h)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
@@ -118,6 +135,21 @@ class ClockSampler:
         except FileNotFoundError:
             self.proc = None
 
+    def begin(self):
+        """Drop the samples taken before the timed region starts."""
+        self.rows.clear()
+
+    def _poll(self):
+        nv, h = self.nvml
+        while not self.stop_evt.is_set():
+            try:
+                mhz = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                bits = int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+                self.rows.append([mhz, self.max_mhz] + ["Active" if bits & b else "Not Active" for b in self.BITS])
+            except Exception:
+                pass
+            self.stop_evt.wait(0.02)
+
     def _read(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
@@ -125,16 +157,26 @@ class ClockSampler:
                 self.rows.append(parts)
 
     def stop(self):
-        if self.proc is None:
+        if self.nvml is not None:
+            self.stop_evt.set()
+            self.thread.join()
+        elif self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        self.proc.wait()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:]) if v.lower() == "active"})
-        mx = next((float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()), None)
+        else:
+            self.proc.terminate()
+            self.proc.wait()
+
+        def num(x):
+            try:
+                return float(x)
+            except (TypeError, ValueError):
+                return None
+
+        sm = [v for v in (num(r[0]) for r in self.rows) if v is not None]
+        reasons = sorted({n for r in self.rows for n, v in zip(self.NAMES, r[2:]) if str(v).lower() == "active"})
+        mx = next((v for v in (num(r[1]) for r in self.rows) if v is not None), None)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(self.rows), "source": "nvml" if self.nvml is not None else "nvidia-smi"}
 
 
 def dist_setup():
@@ -364,10 +406,11 @@ def run_ours(args, world, rank, local):
     barrier(world)
     clocks = ClockSampler(local)
     clocks.start()
-    time.sleep(0.3)
+    time.sleep(0.3)  # (nvidia-smi fallback: let the sampler start)
     torch.cuda.synchronize()
     launches0 = N.LAUNCH_COUNT[0]
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.begin()  # samples count from here (the timed region) on
     ev0.record()
     for _ in range(args.steps):
         res = gstep() if use_graph else step()
@@ -616,6 +659,7 @@ def run_sharded(args, comm, world, rank, sync):
     clocks.start()
     launches0 = N.LAUNCH_COUNT[0]
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.begin()
     ev0.record()
     for _ in range(args.steps):
         res = step(prompt)
