@@ -111,6 +111,9 @@ constexpr uint32_t kPCol0 = 64, kPColGap = 0;  // P over the upper half of S
 constexpr int kThreads = 384;
 constexpr int kWarpTma = 8, kWarpMma = 9, kWarpAlloc = 10;
 #endif
+#ifndef IFKV_ATTN10_OPTMAX
+#define IFKV_ATTN10_OPTMAX 0
+#endif
 #ifndef IFKV_ATTN10_REGS
 #define IFKV_ATTN10_REGS 200
 #endif
@@ -245,6 +248,7 @@ __device__ __forceinline__ void softmax_tile10(Smem10& sm, uint32_t tmem, int x,
 #if IFKV_ATTN10_ONEPASS
     // the whole 128-key S row in registers (one TMEM read)
     float v[128];
+    const float mb_opt = m_used == -INFINITY ? 0.f : m_used * scale_log2;  // offset before this block's max
 #pragma unroll
     for (int q = 0; q < 4; ++q) tc::tmem_ld32(t_s + 32 * q, v + 32 * q);
     tc::tmem_ld_wait();
@@ -307,7 +311,8 @@ __device__ __forceinline__ void softmax_tile10(Smem10& sm, uint32_t tmem, int x,
     // each 64-key half's exponentials are stored and published as soon as
     // they exist, so PV_x(j) on keys 0..63 overlaps the exponentials of keys
     // 64..127 (the whole S row was read before P overwrites its upper half)
-    if (j > 0 && __any_sync(0xffffffffu, need)) {
+    const bool any_need = __any_sync(0xffffffffu, need);
+    if (j > 0 && any_need) {
       const float a = need ? alpha : 1.f;
 #pragma unroll 1
       for (int c = 0; c < kDh / 32; ++c) {
@@ -320,13 +325,11 @@ __device__ __forceinline__ void softmax_tile10(Smem10& sm, uint32_t tmem, int x,
       }
     }
     constexpr int kPairs = 64 / kParts;  // column pairs (= TMEM columns of P) per published part
-#pragma unroll
-    for (int hf = 0; hf < kParts; ++hf) {
-      uint32_t p[kPairs];
+    auto exps = [&](int hf, float2 off, uint32_t* p) {
 #pragma unroll
       for (int u = 0; u < kPairs; ++u) {
         const int pu = hf * kPairs + u;  // column pair pu = keys 2pu, 2pu+1
-        const float2 xx = tc::ffma2(make_float2(v[2 * pu], v[2 * pu + 1]), sc2, mb2);
+        const float2 xx = tc::ffma2(make_float2(v[2 * pu], v[2 * pu + 1]), sc2, off);
         float2 e;
         if (((IFKV_ATTN10_FRAGS >> (pu >> 4)) & 1) && (pu & 7) >= 8 - IFKV_ATTN10_EMU)
           e = tc::ex2_poly2(xx);
@@ -335,6 +338,26 @@ __device__ __forceinline__ void softmax_tile10(Smem10& sm, uint32_t tmem, int x,
         sum2[u & 1] = tc::fadd2(sum2[u & 1], e);
         p[u] = tc::pack_bf16(e.x, e.y);
       }
+    };
+#pragma unroll
+    for (int hf = 0; hf < kParts; ++hf) {
+      uint32_t p[kPairs];
+#if IFKV_ATTN10_OPTMAX
+      // part 0 with the offset from before this block: independent of the row
+      // max, so it overlaps the max reduction; the offset is unchanged unless
+      // a row's max grew by > 2^8 (then redone with the new one)
+      if (hf == 0) {
+        exps(0, make_float2(-mb_opt, -mb_opt), p);
+        if (any_need) {
+          sum2[0] = sum2[1] = make_float2(0.f, 0.f);
+          exps(0, mb2, p);
+        }
+      } else {
+        exps(hf, mb2, p);
+      }
+#else
+      exps(hf, mb2, p);
+#endif
       if constexpr (kPairs == 32)
         tmem_st32u(t_p + kPairs * hf, p);
       else
