@@ -1,5 +1,5 @@
 """clock64 trace of one v10 attention CTA (the heaviest pair of kv head 0) at
-the C2 shape.  Build: python tools/build_variants.py v10t=IFKV_ATTN_GEN=10,IFKV_ATTN10_TRACE=1
+the C2 shape.  Build: python tools/build_variants.py v10t=IFKV_ATTN10_TRACE=1
 Usage: python tools/attn10_trace.py _ab/v10t/libifkv.so"""
 import ctypes
 import sys
