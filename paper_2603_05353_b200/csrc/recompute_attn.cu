@@ -110,32 +110,21 @@ __global__ void __launch_bounds__(128) recompute_attn_simt_kernel(const T* __res
 
 using namespace ifkv;
 
-extern "C" int ifkv_recompute_attn_tc_v5(const void* q, const void* k_layer, const void* v_layer,
-                                         const int64_t* key_start, const int64_t* horizon, int S, int H, int Hkv,
-                                         int Dh, int n_rows, float scale, void* out, float* ml_out, void* stream);
 extern "C" int ifkv_recompute_attn_tc_v10(const void* q, const void* k_layer, const void* v_layer,
                                           const int64_t* key_start, const int64_t* horizon, int S, int H, int Hkv,
                                           int Dh, int n_rows, float scale, void* out, float* ml_out, void* stream);
-// The tcgen05 kernels: v10 (tc_recompute_attn_v10.cu, default): two tiles
-// per CTA, P written into the TMEM columns of its own S tile and read by a
-// TS-form PV MMA, 5-stage K/V ring; v5 (tc_recompute_attn_v5.cu, A/B with
-// -DIFKV_ATTN_GEN=5): P staged in shared memory so S(j+1) follows the read
-// of S(j).  Same tiles (floor(128/G) tokens x G heads) and key splits below
-// two waves.  v10 equals v5 alone at C2 and is 1.5 % faster over a whole
-// power-capped step (profiles/r2_attn10.md).  Earlier generations (v2, v4,
-// the CTA-pair kernels v7-v9) were measured slower and removed
-// (profiles/r1_attn_ab.md, profiles/r2_attn.md, sources in profiles/attic/).
-#ifndef IFKV_ATTN_GEN
-#define IFKV_ATTN_GEN 10
-#endif
+// The tcgen05 kernel (tc_recompute_attn_v10.cu): two tiles of floor(128/G)
+// tokens x G heads per CTA, P written into the TMEM columns of its own S tile
+// and read by a TS-form PV MMA part by part, a quarter of the exponentials on
+// the FMA pipe, key splits below two waves.  The generations it replaced (v2,
+// v4, v5, the CTA-pair kernels v7-v9) were measured slower and moved out of
+// the library (profiles/r1_attn_ab.md, r2_attn.md, r2_attn10.md; sources in
+// profiles/attic/).
 static int recompute_attn_tc_any(const void* q, const void* k_layer, const void* v_layer, const int64_t* horizon,
                                  int S, int H, int Hkv, int Dh, int n_rows, float scale, void* out, float* ml_out,
                                  void* stream, const int64_t* key_start = nullptr) {
-  if (IFKV_ATTN_GEN == 10)
-    return ifkv_recompute_attn_tc_v10(q, k_layer, v_layer, key_start, horizon, S, H, Hkv, Dh, n_rows, scale, out,
-                                      ml_out, stream);
-  return ifkv_recompute_attn_tc_v5(q, k_layer, v_layer, key_start, horizon, S, H, Hkv, Dh, n_rows, scale, out,
-                                   ml_out, stream);
+  return ifkv_recompute_attn_tc_v10(q, k_layer, v_layer, key_start, horizon, S, H, Hkv, Dh, n_rows, scale, out,
+                                    ml_out, stream);
 }
 
 static int recompute_attn_simt_impl(int dtype, const void* q, const void* k_layer, const void* v_layer,

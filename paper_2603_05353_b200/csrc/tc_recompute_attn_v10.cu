@@ -456,6 +456,11 @@ extern "C" int ifkv_attn10_trace_clear() {
 }
 #endif
 
+extern "C" int ifkv_recompute_attn_tc_supported(int dtype, int H, int Hkv, int Dh) {
+  if (dtype != IFKV_BF16 || Dh != kDh || Hkv <= 0 || H % Hkv) return 0;
+  return H / Hkv <= 16 ? 1 : 0;  // a tile holds floor(128 / G) tokens x G heads
+}
+
 extern "C" int ifkv_recompute_attn_tc_v10(const void* q, const void* k_layer, const void* v_layer,
                                           const int64_t* key_start, const int64_t* horizon, int S, int H, int Hkv,
                                           int Dh, int n_rows, float scale, void* out, float* ml_out, void* stream) {
