@@ -1,5 +1,6 @@
 // ABI bookkeeping: thread-local error message and version.
 #include <stdarg.h>
+#include <stdlib.h>
 
 #include <mutex>
 
@@ -13,6 +14,14 @@ void set_error(const char* fmt, ...) {
   va_start(ap, fmt);
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("IFKV_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 void* workspace_alloc(size_t bytes, cudaStream_t st) {

@@ -80,6 +80,8 @@ __global__ void __launch_bounds__(kThreads) add_rmsnorm_kernel(float* __restrict
                                                                int n_parts, const float* __restrict__ gain, int rows,
                                                                int d, int mode, void* __restrict__ out) {
   __shared__ float red[kThreads / 32];
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   float* hr = h + (int64_t)r * d;
   const int64_t pstride = (int64_t)rows * d;
@@ -186,6 +188,8 @@ __device__ __forceinline__ float silu_f(float g) {
 template <typename T>
 __global__ void silu_mul_kernel(const T* __restrict__ gu, int n_parts, int rows, int d_ff, int blk, int mode,
                                 void* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int vpr = d_ff / 4;
   const int64_t nv = (int64_t)rows * vpr;
   const int64_t pstride = (int64_t)rows * 2 * d_ff;
@@ -364,8 +368,9 @@ extern "C" int ifkv_add_rmsnorm(float* h, const void* delta, int delta_dtype, in
       add_rmsnorm_kernel<__nv_bfloat16, 1024, 2><<<rows, 1024, 0, s>>>(h, (const __nv_bfloat16*)delta, n_parts, gain,
                                                                       rows, d, out_mode, out);
     else
-      add_rmsnorm_kernel<float, 1024, 2><<<rows, 1024, 0, s>>>(h, (const float*)delta, n_parts, gain, rows, d,
-                                                              out_mode, out);
+      IFKV_CUDA_CALL(launch_pdl(add_rmsnorm_kernel<float, 1024, 2>, dim3(rows), dim3(1024), 0, s, h,
+                                (const float*)delta, n_parts, gain, rows, d, out_mode, out),
+                     "add_rmsnorm: launch");
   } else if (d <= 4096) {
     if (bf)
       add_rmsnorm_kernel<__nv_bfloat16, 128><<<rows, 128, 0, s>>>(h, (const __nv_bfloat16*)delta, n_parts, gain, rows,
@@ -412,8 +417,9 @@ extern "C" int ifkv_silu_mul(const void* gu, int gu_dtype, int n_parts, int rows
     silu_mul_kernel<__nv_bfloat16><<<grid, 256, 0, as_stream(stream)>>>((const __nv_bfloat16*)gu, n_parts, rows,
                                                                        d_ff, gu_block, out_mode, out);
   else
-    silu_mul_kernel<float><<<grid, 256, 0, as_stream(stream)>>>((const float*)gu, n_parts, rows, d_ff, gu_block,
-                                                               out_mode, out);
+    IFKV_CUDA_CALL(launch_pdl(silu_mul_kernel<float>, dim3(grid), dim3(256), 0, as_stream(stream), (const float*)gu,
+                              n_parts, rows, d_ff, gu_block, out_mode, out),
+                   "silu_mul: launch");
   IFKV_LAUNCH_CHECK("silu_mul");
   return IFKV_OK;
 }

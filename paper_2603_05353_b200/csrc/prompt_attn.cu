@@ -134,6 +134,8 @@ __global__ void __launch_bounds__(256) prompt_attn_merge_kernel(
     __nv_bfloat16* __restrict__ ctx3, int64_t plane) {
   __shared__ float s_m[8], s_l[8];
   __shared__ float s_o[8][256];
+  pdl_trigger();  // the next projection (programmatic launch) may start streaming its weights
+  pdl_wait();
   const int r = blockIdx.x;  // (g, h, m)
   const int m = r % M, h = (r / M) % H, g = r / (M * H);
   const int b = item_begin[g], e = item_begin[g + 1];

@@ -175,6 +175,8 @@ __global__ void prompt_qkv_kernel(const float* __restrict__ qkv, int n_parts, in
                                   const int32_t* __restrict__ qset_cs, const float2* __restrict__ cs_delta,
                                   float* __restrict__ kp, float* __restrict__ vp, float* __restrict__ qd,
                                   __nv_bfloat16* __restrict__ qd3) {
+  pdl_trigger();
+  pdl_wait();
   const int half = Dh / 2;
   const int width_pairs = (H + 2 * Hkv) * half;
   const int rows = G * M;
@@ -546,9 +548,11 @@ extern "C" int ifkv_prompt_qkv(const float* qkv, int n_parts, int G, int M, int 
   // grid.y: slabs of kQsetsPerThread query sets (n_qsets bounds every group's
   // count; slabs past a group's end return at once)
   const dim3 grid((unsigned)((total + 255) / 256), (unsigned)((n_qsets + kQsetsPerThread - 1) / kQsetsPerThread));
-  prompt_qkv_kernel<<<grid, 256, 0, as_stream(stream)>>>(
-      qkv, n_parts, part_stride, G, M, H, Hkv, Dh, reinterpret_cast<const float2*>(cs), qs_begin, qs_list, qset_cs,
-      reinterpret_cast<const float2*>(cs_delta), kp, vp, qd, reinterpret_cast<__nv_bfloat16*>(qd3));
+  IFKV_CUDA_CALL(launch_pdl(prompt_qkv_kernel, grid, dim3(256), 0, as_stream(stream), qkv, n_parts, part_stride, G, M,
+                            H, Hkv, Dh, reinterpret_cast<const float2*>(cs), qs_begin, qs_list, qset_cs,
+                            reinterpret_cast<const float2*>(cs_delta), kp, vp, qd,
+                            reinterpret_cast<__nv_bfloat16*>(qd3)),
+                 "prompt_qkv: launch");
   IFKV_LAUNCH_CHECK("prompt_qkv");
   return IFKV_OK;
 }

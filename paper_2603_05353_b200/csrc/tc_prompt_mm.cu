@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(128, 2)
   const int s0 = (int)((int64_t)blockIdx.y * k_steps / gridDim.y);
   const int ns = (int)((int64_t)(blockIdx.y + 1) * k_steps / gridDim.y) - s0;
 
+  pdl_trigger();
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
       tc::mbar_init(&full[i], 1);
@@ -57,7 +58,18 @@ __global__ void __launch_bounds__(128, 2)
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tm_w);
     tc::tma_prefetch(&tm_x);
-    for (int i = 0; i < ns; ++i) {
+    // the weights do not depend on the previous kernel: the first stages'
+    // W tiles are requested before waiting for it (programmatic launch),
+    // the activations after
+    const int pre = ns < kStages ? ns : kStages;
+    for (int i = 0; i < pre; ++i) {
+      tc::mbar_arrive_expect_tx(&full[i], kWStage + x_bytes);
+      tc::tma_load_2d(base + i * stage_bytes, &tm_w, &full[i], (s0 + i) * kKStep, n0);
+    }
+    pdl_wait();
+    for (int i = 0; i < pre; ++i)
+      tc::tma_load_2d(base + i * stage_bytes + kWStage, &tm_x, &full[i], (s0 + i) * kKStep, 0);
+    for (int i = pre; i < ns; ++i) {
       const int s = i % kStages;
       const int k0 = (s0 + i) * kKStep;
       tc::mbar_wait(&empty[s], ((i / kStages) & 1) ^ 1);
@@ -148,7 +160,9 @@ extern "C" int ifkv_prompt_mm(const void* x, int P, int R, int K, const void* w,
   auto kern = prompt_mm_kernel<kStages>;
   IFKV_CUDA_CALL(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                  "prompt_mm: smem attribute");
-  kern<<<dim3(N / kN, splits), 128, smem, as_stream(stream)>>>(tw, tx, P, R, NR, k_steps, N, out);
+  IFKV_CUDA_CALL(launch_pdl(kern, dim3(N / kN, splits), dim3(128), smem, as_stream(stream), tw, tx, P, R, NR, k_steps,
+                            N, out),
+                 "prompt_mm: launch");
   IFKV_LAUNCH_CHECK("prompt_mm");
   return IFKV_OK;
 }
