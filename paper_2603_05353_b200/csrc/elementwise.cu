@@ -131,6 +131,8 @@ __global__ void __launch_bounds__(256) add_rmsnorm_pf_kernel(float* __restrict__
                                                              int mode, void* __restrict__ out) {
   constexpr int d = 4096, kV = 4;
   __shared__ float red[2][8];
+  pdl_trigger();
+  pdl_wait();
   const int64_t pstride = (int64_t)rows * d;
   float4 g[kV];
 #pragma unroll
@@ -359,10 +361,13 @@ extern "C" int ifkv_add_rmsnorm(float* h, const void* delta, int delta_dtype, in
   if (IFKV_RMS_PERSIST && d == 4096 && rows >= 148 * 4) {
     const unsigned grid = 148 * IFKV_RMS_PERSIST_CTAS;
     if (bf)
-      add_rmsnorm_pf_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(h, (const __nv_bfloat16*)delta, n_parts, gain, rows,
-                                                                out_mode, out);
+      IFKV_CUDA_CALL(launch_pdl(add_rmsnorm_pf_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, s, h,
+                                (const __nv_bfloat16*)delta, n_parts, gain, rows, out_mode, out),
+                     "add_rmsnorm: launch");
     else
-      add_rmsnorm_pf_kernel<float><<<grid, 256, 0, s>>>(h, (const float*)delta, n_parts, gain, rows, out_mode, out);
+      IFKV_CUDA_CALL(launch_pdl(add_rmsnorm_pf_kernel<float>, dim3(grid), dim3(256), 0, s, h, (const float*)delta,
+                                n_parts, gain, rows, out_mode, out),
+                     "add_rmsnorm: launch");
   } else if (rows < 2 * 148 && d <= 4 * 2 * 1024) {  // few rows (prompt forward): spread each row over 1024 threads
     if (bf)
       add_rmsnorm_kernel<__nv_bfloat16, 1024, 2><<<rows, 1024, 0, s>>>(h, (const __nv_bfloat16*)delta, n_parts, gain,

@@ -198,6 +198,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<BM, BN>::kThread
   uint64_t* tempty = tfull + 2;  // [kBufs] accumulator drained (leader; every epilogue warp of both CTAs arrives)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
+  pdl_trigger();
   const int warp = threadIdx.x >> 5;
   const uint32_t rank = cluster_rank();
   const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
@@ -228,6 +229,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<BM, BN>::kThread
       tc::tma_prefetch(&tm_w);
       const uint32_t full0 = map_to_rank(full, 0);
       int it = 0;
+      // programmatic launch: the weights of the first stages do not depend on
+      // the previous kernel and are requested before waiting for it; the
+      // activations (its output) after
+      int pre = 0;
+      if (pair < n_tile_total) {
+        int mt, nt;
+        tile_mn(pair, m_tiles, n_tiles, band, mt, nt);
+        const int w0 = nt * BN + (int)rank * (BN / 2);
+        pre = k_steps < S ? k_steps : S;
+        for (int ks = 0; ks < pre; ++ks) {
+          if (rank == 0) tc::mbar_arrive_expect_tx(&full[ks], 2 * C::kStage);
+          tma_load_2d_pair(base + ks * C::kStage + C::kAStage, &tm_w, full0 + (uint32_t)(ks * 8), ks * kBK, w0);
+        }
+      }
+      pdl_wait();
       for (int t = pair; t < n_tile_total; t += n_pairs) {
         int mt, nt;
         tile_mn(t, m_tiles, n_tiles, band, mt, nt);
@@ -235,10 +251,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<BM, BN>::kThread
         const int w0 = nt * BN + (int)rank * (BN / 2);
         for (int ks = 0; ks < k_steps; ++ks, ++it) {
           const int s = it % S;
-          tc::mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
-          uint8_t* st = base + s * C::kStage;
-          if (rank == 0) tc::mbar_arrive_expect_tx(&full[s], 2 * C::kStage);
           const uint32_t bar = full0 + (uint32_t)(s * 8);
+          uint8_t* st = base + s * C::kStage;
+          if (it < pre) {  // W already requested
+            tma_load_2d_pair(st, &tm_a, bar, ks * kBK, m0);
+            continue;
+          }
+          tc::mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+          if (rank == 0) tc::mbar_arrive_expect_tx(&full[s], 2 * C::kStage);
           tma_load_2d_pair(st, &tm_a, bar, ks * kBK, m0);
           tma_load_2d_pair(st + C::kAStage, &tm_w, bar, ks * kBK, w0);
         }
@@ -402,7 +422,9 @@ int launch_tile(const void* a, int64_t lda, int M, int K, const void* w, int N, 
   const int pairs = std::min(m_tiles * n_tiles, sm_count() / 2);
   auto kern = gemm_pair_kernel<BM, BN, EPI>;
   IFKV_CUDA_CALL(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem), "gemm: smem");
-  kern<<<2 * pairs, C::kThreads, C::kSmem, st>>>(ta, tw, to, M, N, K, m_tiles, n_tiles, band, p);
+  IFKV_CUDA_CALL(launch_pdl(kern, dim3(2 * pairs), dim3(C::kThreads), C::kSmem, st, ta, tw, to, M, N, K, m_tiles,
+                            n_tiles, band, p),
+                 "gemm: launch");
   IFKV_LAUNCH_CHECK("gemm");
   return IFKV_OK;
 }

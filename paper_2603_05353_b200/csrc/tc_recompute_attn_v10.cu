@@ -265,6 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                               __nv_bfloat16* __restrict__ out, float* __restrict__ ml_out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem10& sm = *reinterpret_cast<Smem10*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = H / Hkv;
   const int tok = kRows / G;
@@ -325,6 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::tma_prefetch(&tm_q);
       tc::tma_prefetch(&tm_k);
       tc::tma_prefetch(&tm_v);
+      pdl_wait();  // Q and the slab's fresh K/V rows come from the previous kernel
       tc::mbar_arrive_expect_tx(&sm.q_full, (nB > 0 ? 2 : 1) * 2 * tok * G * 128);
       tc::tma_load_4d(sm.q[0], &tm_q, &sm.q_full, 0, 0, g, tA);
       tc::tma_load_4d(sm.q[0] + kPanel, &tm_q, &sm.q_full, 64, 0, g, tA);
@@ -398,6 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     tc::reg_alloc<kSoftmaxRegs>();
+    pdl_wait();  // (tiles without key blocks write their rows without any other wait)
     const int x = warp >> 2;
     const int nx = x == 0 ? nA : nB;
     const int tx = x == 0 ? tA : tB;
@@ -500,8 +503,9 @@ extern "C" int ifkv_recompute_attn_tc_v10(const void* q, const void* k_layer, co
   if (Hkv * pairs < IFKV_ATTN10_SPLIT_WAVES * sms)
     P = min(IFKV_ATTN10_SPLIT_MAX, (IFKV_ATTN10_SPLIT_WAVES * sms + Hkv * pairs - 1) / (Hkv * pairs));
   if (P == 1) {
-    recompute_attn_v10_kernel<<<dim3(Hkv, pairs, 1), kThreads, smem, st>>>(tq, tk, tv, horizon, key_start, S, H, Hkv,
-                                                                      scale_log2, (__nv_bfloat16*)out, ml_out);
+    IFKV_CUDA_CALL(launch_pdl(recompute_attn_v10_kernel, dim3(Hkv, pairs, 1), dim3(kThreads), smem, st, tq, tk, tv,
+                              horizon, key_start, S, H, Hkv, scale_log2, (__nv_bfloat16*)out, ml_out),
+                   "recompute_attn_v10: launch");
     IFKV_LAUNCH_CHECK("recompute_attn_v10");
     return IFKV_OK;
   }
@@ -514,8 +518,9 @@ extern "C" int ifkv_recompute_attn_tc_v10(const void* q, const void* k_layer, co
   }
   auto* part_o = reinterpret_cast<__nv_bfloat16*>(ws);
   auto* part_ml = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + o_bytes);
-  recompute_attn_v10_kernel<<<dim3(Hkv, pairs, P), kThreads, smem, st>>>(tq, tk, tv, horizon, key_start, S, H, Hkv,
-                                                                    scale_log2, part_o, part_ml);
+  IFKV_CUDA_CALL(launch_pdl(recompute_attn_v10_kernel, dim3(Hkv, pairs, P), dim3(kThreads), smem, st, tq, tk, tv,
+                            horizon, key_start, S, H, Hkv, scale_log2, part_o, part_ml),
+                 "recompute_attn_v10: launch (split)");
   IFKV_LAUNCH_CHECK("recompute_attn_v10 (split)");
   attn_v10_merge_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(part_o, part_ml, P, rows, (__nv_bfloat16*)out,
                                                                       ml_out);
