@@ -35,7 +35,7 @@ struct PSmem {
   uint8_t k[2][kTile];
   uint8_t v[2][kTile];  // mode 1: transposed probabilities [128][128] fp32 (64 KB)
   uint64_t q_full, k_full[2], k_empty[2], v_full[2], v_empty[2];
-  uint64_t s_full, s_free, p_full, pv_done;
+  uint64_t s_full, s_free, p_full[2], pv_done;  // p_full: P published by 64-key halves
   uint32_t tmem_base;
 };
 
@@ -69,7 +69,8 @@ __global__ void __launch_bounds__(192, 1)
     }
     tc::mbar_init(&sm.s_full, 1);
     tc::mbar_init(&sm.s_free, 128);
-    tc::mbar_init(&sm.p_full, 128);
+    tc::mbar_init(&sm.p_full[0], 128);
+    tc::mbar_init(&sm.p_full[1], 128);
     tc::mbar_init(&sm.pv_done, 1);
     tc::fence_barrier_init();
   }
@@ -136,17 +137,22 @@ __global__ void __launch_bounds__(192, 1)
         if (j + 1 < nblk) issue_s(j + 1);
         if constexpr (kMode == 0) {
           const int s = j & 1;
-          tc::mbar_wait(&sm.p_full, j & 1);
           tc::mbar_wait(&sm.v_full[s], (j >> 1) & 1);
-          tc::tc_fence_after();
           const uint32_t v_addr = tc::smem_u32(sm.v[s]);
+          // PV by 64-key halves as the softmax publishes them (fixed order:
+          // half, term, key step)
 #pragma unroll
-          for (int t = 0; t < 3; ++t) {
+          for (int hf = 0; hf < 2; ++hf) {
+            tc::mbar_wait(&sm.p_full[hf], j & 1);
+            tc::tc_fence_after();
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-              uint64_t b = tc::smem_desc_sw128(v_addr + kk * 2048, kPanel, 1024);
-              tc::mma_bf16_ts(tmem + kColO, tmem + kColP + 64 * t + 8 * kk, b, idesc_pv,
-                              (j > 0 || t > 0 || kk > 0) ? 1u : 0u);
+            for (int t = 0; t < 3; ++t) {
+#pragma unroll
+              for (int kk = 4 * hf; kk < 4 * hf + 4; ++kk) {
+                uint64_t b = tc::smem_desc_sw128(v_addr + kk * 2048, kPanel, 1024);
+                tc::mma_bf16_ts(tmem + kColO, tmem + kColP + 64 * t + 8 * kk, b, idesc_pv,
+                                (j > 0 || t > 0 || kk > 0) ? 1u : 0u);
+              }
             }
           }
           tc::mma_commit(&sm.pv_done);
@@ -219,33 +225,38 @@ __global__ void __launch_bounds__(192, 1)
         // P(j-1) consumed and O = PV(0..j-1) complete
         if (j > 0) tc::mbar_wait(&sm.pv_done, (j - 1) & 1);
         tc::tc_fence_after();
-        // P = hi + mid + lo (bf16 pairs), term t at TMEM cols kColP + 64 t + key / 2
+        // P = hi + mid + lo (bf16 pairs), term t at TMEM cols kColP + 64 t + key / 2,
+        // published by 64-key halves so PV on keys 0..63 overlaps the second half
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {  // 8-column stores keep the split terms' registers low (no spills)
-          uint32_t p0[8], p1[8], p2[8];
+        for (int hf = 0; hf < 2; ++hf) {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) tc::split3_pair(v[16 * q + 2 * u], v[16 * q + 2 * u + 1], p0[u], p1[u], p2[u]);
-          tc::tmem_st8(tmem + lane_off + kColP + 0 * 64 + 8 * q, p0);
-          tc::tmem_st8(tmem + lane_off + kColP + 1 * 64 + 8 * q, p1);
-          tc::tmem_st8(tmem + lane_off + kColP + 2 * 64 + 8 * q, p2);
-        }
-        // O rescale after the P terms are out of registers (v[] dead: no spills)
-        if (j > 0 && __any_sync(0xffffffffu, need)) {
-          const float a = need ? alpha : 1.f;
-#pragma unroll 1
-          for (int c = 0; c < 8; ++c) {
-            float o[16];
-            tc::tmem_ld16(tmem + lane_off + kColO + c * 16, o);
-            tc::tmem_ld_wait();
+          for (int q = 4 * hf; q < 4 * hf + 4; ++q) {  // 8-column stores keep the split terms' registers low
+            uint32_t p0[8], p1[8], p2[8];
 #pragma unroll
-            for (int u = 0; u < 16; ++u) o[u] *= a;
-            tc::tmem_st16(tmem + lane_off + kColO + c * 16, reinterpret_cast<const uint32_t*>(o));
+            for (int u = 0; u < 8; ++u)
+              tc::split3_pair(v[16 * q + 2 * u], v[16 * q + 2 * u + 1], p0[u], p1[u], p2[u]);
+            tc::tmem_st8(tmem + lane_off + kColP + 0 * 64 + 8 * q, p0);
+            tc::tmem_st8(tmem + lane_off + kColP + 1 * 64 + 8 * q, p1);
+            tc::tmem_st8(tmem + lane_off + kColP + 2 * 64 + 8 * q, p2);
           }
+          // O rescale before the first PV of this block reads O
+          if (hf == 0 && j > 0 && __any_sync(0xffffffffu, need)) {
+            const float a = need ? alpha : 1.f;
+#pragma unroll 1
+            for (int c = 0; c < 8; ++c) {
+              float o[16];
+              tc::tmem_ld16(tmem + lane_off + kColO + c * 16, o);
+              tc::tmem_ld_wait();
+#pragma unroll
+              for (int u = 0; u < 16; ++u) o[u] *= a;
+              tc::tmem_st16(tmem + lane_off + kColO + c * 16, reinterpret_cast<const uint32_t*>(o));
+            }
+          }
+          tc::tmem_st_wait();
+          tc::tc_fence_before();
+          tc::mbar_arrive(&sm.p_full[hf]);
         }
         l = l * alpha + sum;
-        tc::tmem_st_wait();
-        tc::tc_fence_before();
-        tc::mbar_arrive(&sm.p_full);
       } else {
         // p = exp(s - m_final) / l_final -> transposed smem -> column sums
         asm volatile("bar.sync 1, 128;" ::: "memory");  // previous block's column reads done
