@@ -76,9 +76,6 @@ constexpr int kPairs = 64 / kParts;  // column pairs (= TMEM columns of P) per p
 #ifndef IFKV_ATTN10_TRACE
 #define IFKV_ATTN10_TRACE 0
 #endif
-#ifndef IFKV_ATTN10_LATESUM2
-#define IFKV_ATTN10_LATESUM2 0
-#endif
 #if IFKV_ATTN10_TRACE
 // clock64 event trace of ONE CTA (blockIdx 0, 0, 0) for tools/attn10_trace.py:
 // [event][tile][block]; events 0 S observed, 1 row max done, 2 exponentials
@@ -210,12 +207,7 @@ __device__ __forceinline__ void softmax_tile10(Smem10& sm, uint32_t tmem, int x,
           e = tc::ex2_poly2(xx);  // FMA pipe (exactly 0 for masked keys)
         else
           e = make_float2(tc::ex2(xx.x), tc::ex2(xx.y));
-#if IFKV_ATTN10_LATESUM2
-        v[2 * pu] = e.x;  // summed after the last part is published
-        v[2 * pu + 1] = e.y;
-#else
         sum2[u & 1] = tc::fadd2(sum2[u & 1], e);
-#endif
         p[u] = tc::pack_bf16(e.x, e.y);
       }
       if constexpr (kPairs == 32)
@@ -229,10 +221,6 @@ __device__ __forceinline__ void softmax_tile10(Smem10& sm, uint32_t tmem, int x,
     }
     TRACE10(2, x, j);
     TRACE10(3, x, j);
-#if IFKV_ATTN10_LATESUM2
-#pragma unroll
-    for (int u = 0; u < 64; ++u) sum2[u & 1] = tc::fadd2(sum2[u & 1], make_float2(v[2 * u], v[2 * u + 1]));
-#endif
     l = l * alpha + ((sum2[0].x + sum2[1].x) + (sum2[0].y + sum2[1].y));
   }
   if (nblk > 0) {
