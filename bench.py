@@ -395,6 +395,21 @@ def run_ours(args, world, rank, local):
     gem = [(a.elapsed_time(b), w) for a, b, w in prof.get("gemm", [])]
     pmm = [(a.elapsed_time(b), w) for a, b, w in prof.get("prompt_mm", [])]
     del res
+    # the same selection in the float64 scoring mode (exact.py, untimed): how
+    # many near-tied pairs the fp32-accurate fast path orders differently from
+    # a float64 scorer at this instance (the reference scores in float64)
+    sel_parity = None
+    if not args.reorder and world == 1:
+        t64 = time.perf_counter()
+        r64 = P.assemble_select_recompute(weights, chunk_kvs, chunks, prompt,
+                                          P.SelectionConfig(ratio=args.ratio, score_precision="fp64"))
+        torch.cuda.synchronize()
+        s64 = r64.selection.selected_numpy()
+        sel_parity = {"k": int(sel_h.size), "swapped_pairs_vs_fp64_scoring": int(np.setxor1d(sel_h, s64).size // 2),
+                      "fp64_query_ms": (time.perf_counter() - t64) * 1e3,
+                      "note": "score_precision='fp64' reproduces the float64 reference's set at any margin "
+                              "(tests/test_gpu_headline.py); the timed path scores fp32-accurately"}
+        del r64
 
     if use_graph:  # capture (first call) + warm replays, after the eager stage / kernel-bracket passes
         for _ in range(args.warmup):
@@ -601,6 +616,7 @@ def run_ours(args, world, rank, local):
         "chunk_prefill": cp,
         "ratio_vs_full_prefill": ms / full_ms,
         "boundary_margin": margin,
+        "selection_parity": sel_parity,
         "roofline": roof,
         "roofline_kernel1": rot_roof,
         "roofline_scatter": sct_roof,

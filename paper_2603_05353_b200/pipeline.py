@@ -117,8 +117,13 @@ def _select_from_store(weights, chunk_kvs, chunks, prompt_token_ids, config: Sel
     if overlap:  # the scoring pass does not read the slab being gathered: no wait on it
         hi.wait_event(before)
     with torch.cuda.stream(hi):
-        out = E.prompt_forward(weights, store_k, store_v, [group], capture_layer=nl)
-        scores = out.scores.index_select(0, E.h2d(rows, store_k.device))  # store rows -> context order
+        if config.score_precision == "fp64":
+            from .exact import prompt_scores_f64
+
+            full = prompt_scores_f64(weights, store_k, store_v, group.token_ids, group.positions, group.segments, nl)
+        else:
+            full = E.prompt_forward(weights, store_k, store_v, [group], capture_layer=nl).scores
+        scores = full.index_select(0, E.h2d(rows, store_k.device))  # store rows -> context order
         sel = SelectionResult(scores=scores, selected=select_topk(scores, config.resolve_budget(n)),
                               strategy=config.strategy.value, geometry=geometry.mode.value)
     if overlap:
@@ -130,7 +135,7 @@ def _select_from_store(weights, chunk_kvs, chunks, prompt_token_ids, config: Sel
 
 def _graph_ok(weights, chunk_kvs, selection: SelectionConfig, reorder: bool) -> bool:
     return (not reorder and _shared_store(chunk_kvs) is not None and selection.strategy is Strategy.ATTENTION_NORM
-            and weights.precision == "bf16")
+            and weights.precision == "bf16" and selection.score_precision == "fp32")
 
 
 class QueryGraph:

@@ -70,6 +70,10 @@ class SelectionConfig:
     seed: int = 0
     cacheblend_layers: int = 2
     head_aggregation: str = "mean_over_heads"
+    # attention-norm scores: "fp32" (fp32-accurate tcgen05 scorer, the fast
+    # path) or "fp64" (exact.py: the scoring pass in float64, for selected
+    # sets identical to the float64 reference at any boundary margin)
+    score_precision: str = "fp32"
 
     def __post_init__(self):
         self.strategy = Strategy.parse(self.strategy)
@@ -81,6 +85,8 @@ class SelectionConfig:
             raise ConfigurationError(f"topk must be >= 0, got {self.topk}")
         if self.head_aggregation != "mean_over_heads":
             raise ConfigurationError(f"unsupported head aggregation {self.head_aggregation!r}")
+        if self.score_precision not in ("fp32", "fp64"):
+            raise ConfigurationError(f"score_precision must be 'fp32' or 'fp64', got {self.score_precision!r}")
 
     def resolve_budget(self, n_context: int) -> int:
         k = self.topk if self.topk is not None else math.ceil(self.ratio * n_context)
@@ -123,9 +129,9 @@ def score_from_attention(attention, n_context: int) -> np.ndarray:
 
 
 def score_attention_norm(weights, cache: AssembledCache, prompt_token_ids, positions: PositionAssignment,
-                         norm_layer: int):
+                         norm_layer: int, precision: str = "fp32"):
     """Prompt-conditioned importance of every context token (selection.py:127-169).
-    Returns fp32 [N] on the device."""
+    Returns fp32 [N] on the device (float64 with precision "fp64", exact.py)."""
     cfg = weights.config
     if not 0 <= norm_layer < cfg.n_layers:
         raise ConfigurationError(f"norm_layer {norm_layer} outside [0, {cfg.n_layers})")
@@ -142,6 +148,11 @@ def score_attention_norm(weights, cache: AssembledCache, prompt_token_ids, posit
         raise ConfigurationError("token id outside vocabulary")
     group = E.PromptGroup(prompt, np.asarray(positions.prompt_positions, np.int64),
                           E.segments_from_deltas(target - cache.row_positions[:n]))
+    if precision == "fp64":
+        from .exact import prompt_scores_f64
+
+        return prompt_scores_f64(weights, cache.keys, cache.values, group.token_ids, group.positions, group.segments,
+                                 norm_layer)[:n]
     out = E.prompt_forward(weights, cache.keys, cache.values, [group], capture_layer=norm_layer)
     return out.scores[:n]
 
@@ -257,7 +268,7 @@ def run_selection(weights, chunks: Sequence[ChunkSpec], cache: AssembledCache, p
         geometry = resolve_geometry(config, cache, int(prompt.size), weights.config.max_position)
         assignment = assign_positions(geometry, chunks)
         nl = config.norm_layer if config.norm_layer is not None else default_norm_layer(weights.config.n_layers)
-        scores = score_attention_norm(weights, cache, prompt, assignment, nl)
+        scores = score_attention_norm(weights, cache, prompt, assignment, nl, config.score_precision)
         k = config.resolve_budget(n)
         return SelectionResult(scores=scores, selected=select_topk(scores, k), strategy=config.strategy.value,
                                geometry=geometry.mode.value)

@@ -323,6 +323,8 @@ def sharded_select(weights, shard: Shard, cache: AssembledCache, prompt_token_id
     if config.strategy != Strategy.ATTENTION_NORM:
         raise ConfigurationError(f"sharded selection implements the attention-norm strategy only, got "
                                  f"{config.strategy.value!r}")
+    if config.score_precision != "fp32":
+        raise ConfigurationError("sharded selection scores in the fp32-accurate mode only (score_precision='fp32')")
     geo = config.geometry
     mode = geo.mode if isinstance(geo, GeometryConfig) else (GeometryMode.parse(geo) if geo is not None else None)
     if mode not in (None, GeometryMode.GLOBAL):

@@ -171,3 +171,25 @@ def test_depth_32_layers_c1_width_matches_oracle(cuda):
     print("recomputed-row K/V Frobenius error by layer: " + " ".join(f"{li}:{max(e):.1e}" for li, e in enumerate(frobs)))
     assert max(max(e) for e in frobs) <= 1e-2
     assert max(max(e) for e in errs) <= 1.5e-2
+
+
+@pytest.mark.parametrize("shape", ["llama3_8b"])
+def test_headline_width_fp64_selection_bit_exact(cuda, shape):
+    """score_precision='fp64' (exact.py): the scoring pass in float64 on the
+    GPU reproduces the float64 reference's scores to ~1e-12 and its selected
+    set bit for bit, whatever the boundary margin (selection.py:127-183)."""
+    P, cfg, dw, g, kvs = _shape_case(shape, layers=4)
+    nl = P.default_norm_layer(cfg.n_layers)
+    cache = P.assemble(kvs)
+    res = P.run_selection(dw, g.chunks, cache, g.prompt_token_ids,
+                          P.SelectionConfig(ratio=0.15, score_precision="fp64"))
+    got_scores, got = res.scores_numpy(), res.selected_numpy()
+    ow = oracle_weights(dw, nl + 1)
+    oc = O.assemble([oracle_chunk(c) for c in kvs])
+    scores, sel = O.run_selection(ow, oc, g.prompt_token_ids, ratio=0.15)
+    k = math.ceil(0.15 * 32768)
+    s = np.sort(scores)[::-1]
+    print(f"{shape} fp64: boundary gap {(s[k - 1] - s[k]) / s[k - 1]:.2e} rel, max score rel err "
+          f"{np.max(np.abs(got_scores - scores) / scores):.2e}")
+    np.testing.assert_allclose(got_scores, scores, rtol=1e-10, atol=0)
+    np.testing.assert_array_equal(got, sel)

@@ -455,3 +455,21 @@ def test_query_graph_replays_match_eager(cuda, ratio):
         qg.run(np.zeros(31, np.int64))
     with pytest.raises(P.ConfigurationError):
         qg.run(np.full(32, 5000, np.int64))
+
+
+def test_c1_fp64_selection_matches_oracle(c1):
+    """score_precision='fp64' at BASELINE config 1: float64 scores to ~1e-12 of
+    the oracle's, the same selected set; through run_selection and through the
+    store path of assemble_select_recompute (exact.py)."""
+    P = _pkg()
+    dw, ow, g, kvs = c1
+    cache = P.assemble(kvs)
+    cfg64 = P.SelectionConfig(ratio=0.15, score_precision="fp64")
+    res = P.run_selection(dw, g.chunks, cache, g.prompt_token_ids, cfg64)
+    oc = O.assemble([oracle_chunk(c) for c in kvs])
+    scores, sel = O.run_selection(ow, oc, g.prompt_token_ids, ratio=0.15)
+    np.testing.assert_allclose(res.scores_numpy(), scores, rtol=1e-10, atol=0)
+    np.testing.assert_array_equal(res.selected_numpy(), sel)
+    store = P.prefill_chunks(dw, g.chunks)
+    out = P.assemble_select_recompute(dw, store, g.chunks, g.prompt_token_ids, cfg64, graph=True)  # eager (fp64)
+    np.testing.assert_array_equal(out.selection.selected_numpy(), sel)

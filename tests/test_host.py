@@ -135,3 +135,13 @@ def test_device_ops_fail_loudly_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(Exception):
         P.DeviceWeights.random(P.toy_config(), 0)
+
+
+def test_score_precision_option():
+    import paper_2603_05353_b200 as P
+    from paper_2603_05353_b200.errors import ConfigurationError
+
+    assert P.SelectionConfig(ratio=0.1).score_precision == "fp32"
+    assert P.SelectionConfig(ratio=0.1, score_precision="fp64").score_precision == "fp64"
+    with pytest.raises(ConfigurationError):
+        P.SelectionConfig(ratio=0.1, score_precision="fp16")
