@@ -120,7 +120,7 @@ def _select_from_store(weights, chunk_kvs, chunks, prompt_token_ids, config: Sel
         if config.score_precision == "fp64":
             from .exact import prompt_scores_f64
 
-            full = prompt_scores_f64(weights, store_k, store_v, group.token_ids, group.positions, group.segments, nl)
+            full = prompt_scores_f64(weights, store_k, store_v, [group], nl)
         else:
             full = E.prompt_forward(weights, store_k, store_v, [group], capture_layer=nl).scores
         scores = full.index_select(0, E.h2d(rows, store_k.device))  # store rows -> context order

@@ -151,8 +151,7 @@ def score_attention_norm(weights, cache: AssembledCache, prompt_token_ids, posit
     if precision == "fp64":
         from .exact import prompt_scores_f64
 
-        return prompt_scores_f64(weights, cache.keys, cache.values, group.token_ids, group.positions, group.segments,
-                                 norm_layer)[:n]
+        return prompt_scores_f64(weights, cache.keys, cache.values, [group], norm_layer)[:n]
     out = E.prompt_forward(weights, cache.keys, cache.values, [group], capture_layer=norm_layer)
     return out.scores[:n]
 

@@ -193,3 +193,27 @@ def test_headline_width_fp64_selection_bit_exact(cuda, shape):
           f"{np.max(np.abs(got_scores - scores) / scores):.2e}")
     np.testing.assert_allclose(got_scores, scores, rtol=1e-10, atol=0)
     np.testing.assert_array_equal(got, sel)
+
+
+def test_c3_reorder_64_chunks_fp64_bit_exact(cuda):
+    """reorder_and_reselect(score_precision='fp64') at 64 x 2048 chunks
+    (128K): importances to ~1e-12 of the float64 oracle, the permutation and
+    the second-pass set bit-exact at any margin (reorder.py:116-181)."""
+    import paper_2603_05353_b200 as P
+
+    cfg = dataclasses.replace(P.llama3_8b_config(), n_layers=2)
+    task = P.SyntheticTask(kind="uniform_noise", total_length=131072, fixed_size=2048, prompt_length=32,
+                           vocab_size=cfg.vocab_size)
+    dw = P.DeviceWeights.random(cfg, seed=7, precision="bf16")
+    g = P.generate_task(task, seed=0)
+    kvs = [P.prefill_chunk(dw, c) for c in g.chunks]
+    budget = math.ceil(0.15 * 131072)
+    plan, _, second = P.reorder_and_reselect(dw, g.chunks, g.prompt_token_ids, budget=budget, prefilled=kvs,
+                                             score_precision="fp64")
+    ow = oracle_weights(dw, 2)
+    perm, imps, _, scores, sel = O.reorder_and_reselect(ow, [oracle_chunk(c) for c in kvs], g.prompt_token_ids,
+                                                        budget)
+    np.testing.assert_allclose(plan.chunk_importance, imps, rtol=1e-10)
+    np.testing.assert_array_equal(plan.permutation, perm)
+    np.testing.assert_allclose(second.scores_numpy(), scores, rtol=1e-10, atol=0)
+    np.testing.assert_array_equal(second.selected_numpy(), sel)

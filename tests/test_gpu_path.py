@@ -473,3 +473,15 @@ def test_c1_fp64_selection_matches_oracle(c1):
     store = P.prefill_chunks(dw, g.chunks)
     out = P.assemble_select_recompute(dw, store, g.chunks, g.prompt_token_ids, cfg64, graph=True)  # eager (fp64)
     np.testing.assert_array_equal(out.selection.selected_numpy(), sel)
+
+
+def test_c1_fp64_reorder_matches_oracle(c1):
+    P = _pkg()
+    dw, ow, g, kvs = c1
+    plan, cache, second = P.reorder_and_reselect(dw, g.chunks, g.prompt_token_ids, budget=308, prefilled=kvs,
+                                                 score_precision="fp64")
+    perm, imps, _, scores, sel = O.reorder_and_reselect(ow, [oracle_chunk(c) for c in kvs], g.prompt_token_ids, 308)
+    np.testing.assert_allclose(plan.chunk_importance, imps, rtol=1e-10)
+    np.testing.assert_array_equal(plan.permutation, perm)
+    np.testing.assert_allclose(second.scores_numpy(), scores, rtol=1e-10, atol=0)
+    np.testing.assert_array_equal(second.selected_numpy(), sel)
