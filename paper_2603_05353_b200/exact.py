@@ -134,18 +134,17 @@ def prompt_scores_f64(weights, slab_k, slab_v, groups, capture_layer: int, n_row
             all_v = torch.cat([slab_v[li].index_select(0, rows_t).to(f64), v[sl]], dim=0)
             allowed = torch.ones((M, N + M), dtype=torch.bool, device=dev)
             allowed[:, N:] = causal
-            col = torch.zeros(N, dtype=f64, device=dev) if capture else None
-            for g in range(Hkv):
-                qg = q[sl, g * G:(g + 1) * G, :].permute(1, 0, 2)  # [G, M, Dh]
-                logits = torch.where(allowed[None], (qg @ all_k[:, g, :].t()) / scale, ninf)  # [G, M, N + M]
-                e = torch.exp(logits - logits.amax(dim=-1, keepdim=True))
-                e = torch.where(allowed[None], e, zero)
-                p = e / e.sum(dim=-1, keepdim=True)
-                ctx[sl, g * G:(g + 1) * G, :] = (p @ all_v[:, g, :]).permute(1, 0, 2)
-                if capture:
-                    col += p[:, :, :N].sum(dim=(0, 1))
-            if capture:
-                scores[rows_t] = col / H  # head mean, prompt-row sum (selection.py:108-124)
+            # all kv heads in one batched matmul: [Hkv, G*M, Dh] x [Hkv, Dh, N+M]
+            qg = q[sl].reshape(M, Hkv, G, Dh).permute(1, 2, 0, 3).reshape(Hkv, G * M, Dh)
+            logits = torch.bmm(qg, all_k.permute(1, 2, 0)).view(Hkv, G, M, N + M) / scale
+            logits = torch.where(allowed[None, None], logits, ninf)
+            e = torch.exp(logits - logits.amax(dim=-1, keepdim=True))
+            e = torch.where(allowed[None, None], e, zero)
+            p = e / e.sum(dim=-1, keepdim=True)
+            o = torch.bmm(p.view(Hkv, G * M, N + M), all_v.permute(1, 0, 2))  # [Hkv, G*M, Dh]
+            ctx[sl] = o.view(Hkv, G, M, Dh).permute(2, 0, 1, 3).reshape(M, H, Dh)
+            if capture:  # head mean, prompt-row sum (selection.py:108-124)
+                scores[rows_t] = p[..., :N].sum(dim=(0, 1, 2)) / H
         if capture:
             return scores
         h = h + ctx.reshape(R, d) @ lw.wo.to(f64).t()
