@@ -418,6 +418,39 @@ def test_store_path_fuses_rotation_into_assembly(cuda):
     np.testing.assert_array_equal(rot.row_positions, np.arange(rot.context_length))
 
 
+def test_store_reorder_path_matches_plain_reorder(cuda):
+    """The reorder over chunks of one store slab (the first pass reads every
+    chunk's rows in place, no assembled copy) returns the path over separately
+    prefilled chunks' permutation, importances, first- and second-pass scores
+    and sets and recomputed cache bit for bit, and the oracle's permutation
+    and second-pass set."""
+    import torch
+
+    P = _pkg()
+    task = P.SyntheticTask(**C1_TASK)
+    dw, ow, g = _setup(P.c1_config(), 7, "bf16", task, 0)
+    kvs = P.prefill_chunks(dw, g.chunks)
+    cfg = P.SelectionConfig(ratio=0.15)
+    fused = P.assemble_select_recompute(dw, kvs, g.chunks, g.prompt_token_ids, cfg, reorder=True)
+    plain_kvs = [P.ChunkKV(c.chunk_id, c.token_ids, c.keys.clone(), c.values.clone(), c.prefill_positions,
+                           c.provenance, c.model_fingerprint) for c in kvs]  # no store: reorder_and_reselect
+    plain = P.assemble_select_recompute(dw, plain_kvs, g.chunks, g.prompt_token_ids, cfg, reorder=True)
+    fr, pr = fused.reorder, plain.reorder
+    np.testing.assert_array_equal(fr.permutation, pr.permutation)
+    np.testing.assert_array_equal(fr.chunk_importance, pr.chunk_importance)
+    for a, b in zip(fr.first_pass, pr.first_pass):
+        np.testing.assert_array_equal(a.scores_numpy(), b.scores_numpy())
+        np.testing.assert_array_equal(a.selected_numpy(), b.selected_numpy())
+    np.testing.assert_array_equal(fused.selection.scores_numpy(), plain.selection.scores_numpy())
+    np.testing.assert_array_equal(fused.selection.selected_numpy(), plain.selection.selected_numpy())
+    assert torch.equal(fused.cache.keys, plain.cache.keys) and torch.equal(fused.cache.values, plain.cache.values)
+    np.testing.assert_array_equal(fused.cache.row_positions, plain.cache.row_positions)
+    budget = cfg.resolve_budget(sum(c.local_length for c in g.chunks))
+    perm, _, _, _, sel = O.reorder_and_reselect(ow, [oracle_chunk(c) for c in kvs], g.prompt_token_ids, budget)
+    np.testing.assert_array_equal(fr.permutation, perm)
+    np.testing.assert_array_equal(fused.selection.selected_numpy(), sel)
+
+
 @pytest.mark.parametrize("ratio", [0.15, 0.05])
 def test_query_graph_replays_match_eager(cuda, ratio):
     """The CUDA-graph replay of a whole query (QueryGraph: ~450 launches as
