@@ -183,13 +183,18 @@ __global__ void prompt_qkv_kernel(const float* __restrict__ qkv, int n_parts, in
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)rows * width_pairs) return;
   const int r = (int)(t / width_pairs), c = (int)(t % width_pairs);
+  const int head = c / half, pi = c % half;
+  const int g = r / M, m = r % M;
+  // blockIdx.y: this thread's slab of kQsetsPerThread of the group's query sets
+  const int k0 = qs_begin[g] + blockIdx.y * kQsetsPerThread;
+  const int k1 = min(qs_begin[g + 1], k0 + kQsetsPerThread);
+  if (head >= H ? blockIdx.y != 0 : k0 >= k1) return;  // nothing to write: skip the loads
   const float* src = qkv + (int64_t)r * (H + 2 * Hkv) * Dh + 2 * c;
   float x0 = 0.f, x1 = 0.f;
   for (int p = 0; p < n_parts; ++p) {
     x0 += src[p * part_stride];
     x1 += src[p * part_stride + 1];
   }
-  const int head = c / half, pi = c % half;
   if (head < H + Hkv) {
     const float2 a = cs[(int64_t)r * half + pi];
     const float y0 = x0 * a.x - x1 * a.y, y1 = x0 * a.y + x1 * a.x;
@@ -197,18 +202,13 @@ __global__ void prompt_qkv_kernel(const float* __restrict__ qkv, int n_parts, in
     x1 = y1;
   }
   if (head >= H) {
-    if (blockIdx.y != 0) return;
     float* d = (head < H + Hkv ? kp + ((int64_t)r * Hkv + (head - H)) * Dh
                                : vp + ((int64_t)r * Hkv + (head - H - Hkv)) * Dh) + 2 * pi;
     d[0] = x0;
     d[1] = x1;
     return;
   }
-  const int g = r / M, m = r % M;
   const int64_t plane = (int64_t)H * M * Dh;
-  // blockIdx.y: this thread's slab of kQsetsPerThread of the group's query sets
-  const int k0 = qs_begin[g] + blockIdx.y * kQsetsPerThread;
-  const int k1 = min(qs_begin[g + 1], k0 + kQsetsPerThread);
   for (int k = k0; k < k1; ++k) {
     const int s = qs_list[k], ci = qset_cs[s];
     float y0 = x0, y1 = x1;
