@@ -177,6 +177,13 @@ int ifkv_prompt_attn_partial(int kv_dtype, const float* qd, const void* k_slab, 
 int ifkv_prompt_attn_merge(const float* part_ml, const float* part_o, const int32_t* item_begin, int prompt_item0,
                            int n_prompt_items, int G, int H, int M, int Dh, float* ctx, float* ml, void* ctx_split3,
                            void* stream);
+/* ifkv_prompt_attn_merge with one warp per (g, h, m) row instead of a CTA:
+ * the same contract and item order, for groups of few items (the reorder
+ * first pass); its fp32 sums run in item order, so the two entry points may
+ * differ in the last bits. */
+int ifkv_prompt_attn_merge_rows(const float* part_ml, const float* part_o, const int32_t* item_begin,
+                                int prompt_item0, int n_prompt_items, int G, int H, int M, int Dh, float* ctx,
+                                float* ml, void* ctx_split3, void* stream);
 /* Capture-layer column scores (score_from_attention selection.py:108-124):
  * for each scored item column j, scores[key_row0 + j] =
  * (1/H) sum_h sum_m exp(s_hmj - m_hm) / l_hm, deterministic order. */
@@ -189,10 +196,11 @@ int ifkv_score_columns(int kv_dtype, const float* qd, const void* k_slab, const 
  * of the row's group g (qs_list[qs_begin[g] .. qs_begin[g+1])) qd[s][h][m] =
  * R(-cs_delta[qset_cs[s]]) q (qset_cs < 0: no rotation), qd3 (optional) its
  * bf16 hi/mid/lo terms [n_qsets][3][H][M][Dh]; with qd3 given, qd is written
- * only for the unrotated sets (the SIMT prompt items' input).  n_qsets: the
- * total number of query sets (bounds every group's count). */
+ * only for the unrotated sets (the SIMT prompt items' input).  max_group_qsets:
+ * an upper bound of any group's query-set count (the launch's extent over
+ * query sets; the total count is always a valid bound). */
 int ifkv_prompt_qkv(const float* qkv, int n_parts, int G, int M, int H, int Hkv, int Dh, const float* cs,
-                    const int32_t* qs_begin, const int32_t* qs_list, const int32_t* qset_cs, int n_qsets,
+                    const int32_t* qs_begin, const int32_t* qs_list, const int32_t* qset_cs, int max_group_qsets,
                     const float* cs_delta, float* kp, float* vp, float* qd, void* qd3, void* stream);
 /* Rotated query sets: qd[s] = R(-cs[qset_cs[s]]) q[qset_group[s]], transposed
  * from q [G][M][H][Dh] to [H][M][Dh]; qset_cs[s] < 0 means no rotation.

@@ -40,6 +40,7 @@ SIGNATURES = {
     "ifkv_qkv_rope_scatter": [P, I32, I32, I32, I32, I32, I32, P, I32, P, P, P, P, P],
     "ifkv_prompt_attn_partial": [I32, P, P, P, P, P, P, I32, I32, I32, I32, I32, I32, F32, P, P, P],
     "ifkv_prompt_attn_merge": [P, P, P, I32, I32, I32, I32, I32, I32, P, P, P, P],
+    "ifkv_prompt_attn_merge_rows": [P, P, P, I32, I32, I32, I32, I32, I32, P, P, P, P],
     "ifkv_prompt_attn_tc_supported": [I32, I32, I32, I32, I32],
     "ifkv_prompt_attn_partial_tc": [P, I32, P, P, I32, P, I32, I32, I32, I32, I32, F32, P, P, P],
     "ifkv_score_columns_tc": [P, I32, P, I32, P, I32, I32, P, I32, I32, I32, F32, P, P, P],

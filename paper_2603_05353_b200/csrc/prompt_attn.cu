@@ -200,6 +200,68 @@ __global__ void __launch_bounds__(256) prompt_attn_merge_kernel(
 
 // grid (n_items), 128 threads: thread j owns key column j of the item and
 // sums p over all heads and prompt rows in a fixed order (deterministic).
+// The same merge with one warp per (g, h, m) row (8 rows per CTA): for
+// groups of few items (the reorder first pass: K groups, a chunk's items each),
+// where a CTA per row is launch-bound.  Lane owns Dh/32 (<= 8) dims; items in
+// order.
+__global__ void __launch_bounds__(256) prompt_attn_merge_rows_kernel(
+    const float* __restrict__ part_ml, const float* __restrict__ part_o, const int32_t* __restrict__ item_begin,
+    int prompt_item0, int n_prompt, int G, int H, int M, int Dh, float* __restrict__ ctx, float* __restrict__ ml,
+    __nv_bfloat16* __restrict__ ctx3, int64_t plane) {
+  pdl_trigger();
+  pdl_wait();
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);  // (g, h, m)
+  if (r >= G * H * M) return;
+  const int lane = threadIdx.x & 31;
+  const int m = r % M, h = (r / M) % H, g = r / (M * H);
+  const int b = item_begin[g], e = item_begin[g + 1];
+  const int n = e - b + (prompt_item0 >= 0 ? n_prompt : 0);
+  auto row_of = [&](int k) -> int64_t {
+    const int it = k < e - b ? b + k : prompt_item0 + g * n_prompt + (k - (e - b));
+    return ((int64_t)it * H + h) * M + m;
+  };
+  float mx = -INFINITY;
+  for (int k = lane; k < n; k += 32) mx = fmaxf(mx, part_ml[2 * row_of(k)]);
+  mx = warp_max(mx);
+  const int per = (Dh + 31) / 32;
+  const int d0 = lane * per;
+  float l = 0.f, o[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) o[u] = 0.f;
+  for (int k = 0; k < n; ++k) {
+    const int64_t row = row_of(k);
+    const float mi = part_ml[2 * row];
+    const float a = mi == -INFINITY ? 0.f : expf(mi - mx);
+    l += part_ml[2 * row + 1] * a;
+    const float* src = part_o + row * Dh + d0;
+    if (per == 4 && d0 < Dh) {
+      const float4 v = *reinterpret_cast<const float4*>(src);
+      o[0] += v.x * a; o[1] += v.y * a; o[2] += v.z * a; o[3] += v.w * a;
+    } else {
+      for (int u = 0; u < per; ++u)
+        if (d0 + u < Dh) o[u] += src[u] * a;
+    }
+  }
+  for (int u = 0; u < per; ++u) {
+    const int d = d0 + u;
+    if (d >= Dh) break;
+    const float c = l > 0.f ? o[u] / l : 0.f;
+    const int64_t ci = (((int64_t)g * M + m) * H + h) * Dh + d;
+    ctx[ci] = c;
+    if (ctx3) {
+      __nv_bfloat16 a0, a1, a2;
+      split3(c, a0, a1, a2);
+      ctx3[ci] = a0;
+      ctx3[plane + ci] = a1;
+      ctx3[2 * plane + ci] = a2;
+    }
+  }
+  if (lane == 0) {
+    ml[2 * (((int64_t)g * H + h) * M + m)] = mx;
+    ml[2 * (((int64_t)g * H + h) * M + m) + 1] = l;
+  }
+}
+
 __global__ void __launch_bounds__(128) score_columns_kernel(int kv_dtype, const float* __restrict__ qd,
                                                             const void* __restrict__ k_slab,
                                                             const ifkv_attn_item* __restrict__ items,
@@ -277,6 +339,20 @@ extern "C" int ifkv_prompt_attn_merge(const float* part_ml, const float* part_o,
       part_ml, part_o, item_begin, prompt_item0, n_prompt_items, H, M, Dh, ctx, ml, (__nv_bfloat16*)ctx_split3,
       (int64_t)G * M * H * Dh);
   IFKV_LAUNCH_CHECK("prompt_attn_merge");
+  return IFKV_OK;
+}
+
+extern "C" int ifkv_prompt_attn_merge_rows(const float* part_ml, const float* part_o, const int32_t* item_begin,
+                                           int prompt_item0, int n_prompt_items, int G, int H, int M, int Dh,
+                                           float* ctx, float* ml, void* ctx_split3, void* stream) {
+  IFKV_CHECK_ARG(Dh <= 256 && G > 0, "prompt_attn_merge_rows: bad shape");
+  IFKV_CHECK_ARG(prompt_item0 < 0 || n_prompt_items >= 1, "prompt_attn_merge_rows: n_prompt_items must be >= 1");
+  const int64_t rows = (int64_t)G * H * M;
+  IFKV_CUDA_CALL(launch_pdl(prompt_attn_merge_rows_kernel, dim3((unsigned)((rows + 7) / 8)), dim3(256), 0,
+                            as_stream(stream), part_ml, part_o, item_begin, prompt_item0, n_prompt_items, G, H, M, Dh,
+                            ctx, ml, (__nv_bfloat16*)ctx_split3, (int64_t)G * M * H * Dh),
+                 "prompt_attn_merge_rows: launch");
+  IFKV_LAUNCH_CHECK("prompt_attn_merge_rows");
   return IFKV_OK;
 }
 

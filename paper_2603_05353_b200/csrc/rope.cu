@@ -538,16 +538,18 @@ extern "C" int ifkv_rotate_queries(const float* q, int G, int M, int H, int Dh, 
 }
 
 extern "C" int ifkv_prompt_qkv(const float* qkv, int n_parts, int G, int M, int H, int Hkv, int Dh, const float* cs,
-                               const int32_t* qs_begin, const int32_t* qs_list, const int32_t* qset_cs, int n_qsets,
-                               const float* cs_delta, float* kp, float* vp, float* qd, void* qd3, void* stream) {
+                               const int32_t* qs_begin, const int32_t* qs_list, const int32_t* qset_cs,
+                               int max_group_qsets, const float* cs_delta, float* kp, float* vp, float* qd, void* qd3,
+                               void* stream) {
   IFKV_CHECK_ARG(Dh % 2 == 0 && Hkv > 0 && H > 0 && H % Hkv == 0 && n_parts >= 1 && G > 0 && M > 0,
                  "prompt_qkv: bad shape");
-  IFKV_CHECK_ARG(n_qsets >= 1, "prompt_qkv: n_qsets must be >= 1");
+  IFKV_CHECK_ARG(max_group_qsets >= 1, "prompt_qkv: max_group_qsets must be >= 1");
   const int64_t total = (int64_t)G * M * (H + 2 * Hkv) * (Dh / 2);
   const int64_t part_stride = (int64_t)G * M * (H + 2 * Hkv) * Dh;
-  // grid.y: slabs of kQsetsPerThread query sets (n_qsets bounds every group's
-  // count; slabs past a group's end return at once)
-  const dim3 grid((unsigned)((total + 255) / 256), (unsigned)((n_qsets + kQsetsPerThread - 1) / kQsetsPerThread));
+  // grid.y: slabs of kQsetsPerThread query sets (max_group_qsets bounds every
+  // group's count; slabs past a group's end return before loading)
+  const dim3 grid((unsigned)((total + 255) / 256),
+                  (unsigned)((max_group_qsets + kQsetsPerThread - 1) / kQsetsPerThread));
   IFKV_CUDA_CALL(launch_pdl(prompt_qkv_kernel, grid, dim3(256), 0, as_stream(stream), qkv, n_parts, part_stride, G, M,
                             H, Hkv, Dh, reinterpret_cast<const float2*>(cs), qs_begin, qs_list, qset_cs,
                             reinterpret_cast<const float2*>(cs_delta), kp, vp, qd,

@@ -31,6 +31,7 @@ from .errors import ConfigurationError
 
 ITEM_KEYS = 128  # keys per prompt-attention work item (<= kItemKeysMax)
 PROMPT_ITEM_KEYS = 128  # prompt keys per causal prompt item
+MERGE_ROWS_MAX_ITEMS = int(os.environ.get("IFKV_MERGE_ROWS_MAX_ITEMS", "8"))  # warp-per-row merge up to this many
 
 # Optional CUDA-event brackets around named kernels: {name: [(start, end, work)]}
 # (the benchmark sets this to measure per-launch durations for the roofline).
@@ -549,6 +550,10 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
     n_items, n_qsets = items_np.shape[0], qg_np.size
     qs_list = np.argsort(qg_np, kind="stable").astype(np.int32)  # each group's query sets, contiguous
     qs_begin = np.searchsorted(qg_np[qs_list], np.arange(G + 1)).astype(np.int32)
+    max_group_qsets = max(1, int(np.diff(qs_begin).max()))  # prompt_qkv's launch extent over query sets
+    # merge: a warp per output row when every group has few items (a CTA per row is launch-bound there)
+    merge_items = int(np.diff(ctx_begin_np).max()) + -(-M // PROMPT_ITEM_KEYS)
+    merge_fn = "ifkv_prompt_attn_merge_rows" if merge_items <= MERGE_ROWS_MAX_ITEMS else "ifkv_prompt_attn_merge"
     meta = h2d(np.concatenate([items_np.ravel(), ctx_begin_np, qg_np, qc_np, qs_begin, qs_list]), dev)
     items_p = meta.data_ptr()
     prompt_items_p = items_p + 24 * n_ctx
@@ -590,7 +595,7 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
         x = add_rmsnorm(h, pending, pending_parts, lw.attn_norm, mode)
         qkv = mm_parts(x, lw.wqkv)
         N.call("ifkv_prompt_qkv", N.ptr(qkv), qkv.shape[0], G, M, H, Hkv, Dh, N.ptr(cs_prompt), qsb_p, qsl_p, qc_p,
-               n_qsets, N.ptr(cs_delta), N.ptr(kp), N.ptr(vp), N.ptr(qd), N.ptr(qd3), _s())
+               max_group_qsets, N.ptr(cs_delta), N.ptr(kp), N.ptr(vp), N.ptr(qd), N.ptr(qd3), _s())
         capture = capture_layer is not None and li == capture_layer
         with _Bracket("prompt_attn", li):
             side = include_prompt and use_tc and n_ctx and torch.cuda.is_available()
@@ -620,7 +625,7 @@ def prompt_forward(weights, slab_k, slab_v, groups: Sequence[PromptGroup], captu
                        N.ptr(vp), prompt_items_p, n_items - n_ctx, min(M, PROMPT_ITEM_KEYS), H, Hkv, M, Dh, scale,
                        part_ml.data_ptr() + n_ctx * stride_ml, part_o.data_ptr() + n_ctx * stride_o, _s())
             fuse_split = bf16 and merge_hook is None and not capture
-            N.call("ifkv_prompt_attn_merge", N.ptr(part_ml), N.ptr(part_o), ib_p, n_ctx if include_prompt else -1,
+            N.call(merge_fn, N.ptr(part_ml), N.ptr(part_o), ib_p, n_ctx if include_prompt else -1,
                    -(-M // PROMPT_ITEM_KEYS), G,
                    H, M, Dh, N.ptr(ctx), N.ptr(ml), N.ptr(ctx3) if fuse_split else None, _s())
             if merge_hook is not None:
