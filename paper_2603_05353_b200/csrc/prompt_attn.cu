@@ -121,6 +121,114 @@ __global__ void __launch_bounds__(256) prompt_attn_partial_kernel(
   }
 }
 
+// The same partial for Dh = 128 with 16-byte shared-memory traffic: keys staged
+// with float4 / 8 x bf16 copies (K rows padded to 132 floats: conflict-free
+// LDS.128 per 8-lane phase), each lane's key dot product in float4 steps over
+// 4 accumulators, and the lane's 4 output dims read as one float4 per key in
+// P V.  (The generic kernel reads everything as scalars: ~2.5x the
+// instructions; the reorder first pass runs it for 16 prompt groups.)
+constexpr int kD128 = 128, kKStride = 132;
+__global__ void __launch_bounds__(256) prompt_attn_partial_d128_kernel(
+    int kv_dtype, const float* __restrict__ qd, const void* __restrict__ k_slab, const void* __restrict__ v_slab,
+    const float* __restrict__ k_prompt, const float* __restrict__ v_prompt, const ifkv_attn_item* __restrict__ items,
+    int kmax, int H, int Hkv, int M, float scale, float* __restrict__ part_ml, float* __restrict__ part_o) {
+  extern __shared__ __align__(16) float smem[];
+  const ifkv_attn_item it = items[blockIdx.x];
+  const int g = blockIdx.y;
+  const int grp = H / Hkv;
+  const int n = it.n_keys;
+  float* Ks = smem;                    // [n][132]
+  float* Vs = Ks + kmax * kKStride;    // [n][128]
+  float* Qs = Vs + kmax * kD128;       // [8][128]
+  for (int t = threadIdx.x; t < n * (kD128 / 4); t += blockDim.x) {  // one float4 of K and of V per step
+    const int j = t / (kD128 / 4), c = (t % (kD128 / 4)) * 4;
+    float4 kv4, vv4;
+    if (it.prompt) {
+      const int64_t idx = (((int64_t)it.group * M + it.key_row0 + j) * Hkv + g) * kD128 + c;
+      kv4 = *reinterpret_cast<const float4*>(k_prompt + idx);
+      vv4 = *reinterpret_cast<const float4*>(v_prompt + idx);
+    } else {
+      const int64_t idx = ((int64_t)(it.key_row0 + j) * Hkv + g) * kD128 + c;
+      if (kv_dtype == IFKV_F32) {
+        kv4 = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(k_slab) + idx);
+        vv4 = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(v_slab) + idx);
+      } else {
+        const uint2 ku = *reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(k_slab) + idx);
+        const uint2 vu = *reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(v_slab) + idx);
+        const float2 k0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ku.x));
+        const float2 k1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ku.y));
+        const float2 v0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vu.x));
+        const float2 v1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vu.y));
+        kv4 = make_float4(k0.x, k0.y, k1.x, k1.y);
+        vv4 = make_float4(v0.x, v0.y, v1.x, v1.y);
+      }
+    }
+    *reinterpret_cast<float4*>(Ks + j * kKStride + c) = kv4;
+    *reinterpret_cast<float4*>(Vs + j * kD128 + c) = vv4;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* q = Qs + warp * kD128;
+  const int rows = grp * M;
+  for (int r = blockIdx.z * 8 + warp; r < rows; r += 8 * gridDim.z) {
+    const int h = g * grp + r / M, m = r % M;
+    const float* qsrc = qd + (((int64_t)it.qset * H + h) * M + m) * kD128;
+    *reinterpret_cast<float4*>(q + 4 * lane) = *reinterpret_cast<const float4*>(qsrc + 4 * lane);
+    __syncwarp();
+    float logit[4];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int j = lane + 32 * t;
+      logit[t] = -INFINITY;
+      if (32 * t < n && j < n && (!it.prompt || it.key_row0 + j <= m)) {
+        const float* kr = Ks + j * kKStride;
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll 8
+        for (int d = 0; d < kD128; d += 4) {
+          const float4 qv = *reinterpret_cast<const float4*>(q + d);
+          const float4 kv = *reinterpret_cast<const float4*>(kr + d);
+          a0 = fmaf(qv.x, kv.x, a0);
+          a1 = fmaf(qv.y, kv.y, a1);
+          a2 = fmaf(qv.z, kv.z, a2);
+          a3 = fmaf(qv.w, kv.w, a3);
+        }
+        logit[t] = ((a0 + a1) + (a2 + a3)) * scale;
+      }
+      mx = fmaxf(mx, logit[t]);
+    }
+    mx = warp_max(mx);
+    float p[4], l = 0.f;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      p[t] = logit[t] == -INFINITY ? 0.f : expf(logit[t] - mx);
+      l += p[t];
+    }
+    l = warp_sum(l);
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (32 * t >= n) break;
+      const int jn = min(32, n - 32 * t);
+      for (int jj = 0; jj < jn; ++jj) {
+        const float pj = __shfl_sync(0xffffffffu, p[t], jj);
+        const float4 v = *reinterpret_cast<const float4*>(Vs + (32 * t + jj) * kD128 + 4 * lane);
+        o.x = fmaf(pj, v.x, o.x);
+        o.y = fmaf(pj, v.y, o.y);
+        o.z = fmaf(pj, v.z, o.z);
+        o.w = fmaf(pj, v.w, o.w);
+      }
+    }
+    const int64_t row_id = ((int64_t)blockIdx.x * H + h) * M + m;
+    if (lane == 0) {
+      part_ml[2 * row_id] = mx;
+      part_ml[2 * row_id + 1] = l;
+    }
+    *reinterpret_cast<float4*>(part_o + row_id * kD128 + 4 * lane) = o;
+    __syncwarp();
+  }
+}
+
 // grid (G * H * M), 256 threads = 8 warps: merge the group's items.
 // Items of group g: [item_begin[g], item_begin[g+1]) then, if
 // prompt_item0 >= 0, items prompt_item0 + g * n_prompt + [0, n_prompt) (the
@@ -303,7 +411,11 @@ __global__ void __launch_bounds__(128) score_columns_kernel(int kv_dtype, const 
 
 using namespace ifkv;
 
+#ifndef IFKV_PARTIAL_D128
+#define IFKV_PARTIAL_D128 1
+#endif
 static size_t partial_smem(int Dh, int kmax) { return (size_t)(kmax * (Dh + 1) + kmax * Dh + 8 * Dh) * 4; }
+static size_t partial_d128_smem(int kmax) { return (size_t)(kmax * kKStride + kmax * kD128 + 8 * kD128) * 4; }
 static size_t score_smem(int Dh, int M) { return (size_t)(kItemKeysMax * (Dh + 1) + M * Dh) * 4; }
 
 extern "C" int ifkv_prompt_attn_partial(int kv_dtype, const float* qd, const void* k_slab, const void* v_slab,
@@ -314,18 +426,28 @@ extern "C" int ifkv_prompt_attn_partial(int kv_dtype, const float* qd, const voi
   IFKV_CHECK_ARG(Dh % 2 == 0 && Dh <= 256 && H % Hkv == 0 && M > 0, "prompt_attn_partial: bad shape");
   IFKV_CHECK_ARG(max_keys >= 1 && max_keys <= kItemKeysMax, "prompt_attn_partial: max_keys must be in [1, 128]");
   if (n_items <= 0) return IFKV_OK;
-  size_t sm = partial_smem(Dh, max_keys);
-  IFKV_CUDA_CALL(cudaFuncSetAttribute(prompt_attn_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)sm),
-                 "prompt_attn_partial: smem attribute");
+  const bool d128 = Dh == kD128 && IFKV_PARTIAL_D128;
+  size_t sm = d128 ? partial_d128_smem(max_keys) : partial_smem(Dh, max_keys);
+  if (d128)
+    IFKV_CUDA_CALL(cudaFuncSetAttribute(prompt_attn_partial_d128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)sm),
+                   "prompt_attn_partial: smem attribute");
+  else
+    IFKV_CUDA_CALL(cudaFuncSetAttribute(prompt_attn_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)sm),
+                   "prompt_attn_partial: smem attribute");
   const int rows = (H / Hkv) * M;
   int splits = (rows + 7) / 8;
   const int64_t ctas = (int64_t)n_items * Hkv;
   while (splits > 1 && ctas * splits > 4 * 148) splits = (splits + 1) / 2;  // enough CTAs, bounded restaging
   dim3 grid(n_items, Hkv, splits);
-  prompt_attn_partial_kernel<<<grid, 256, sm, as_stream(stream)>>>(kv_dtype, qd, k_slab, v_slab, k_prompt,
-                                                                     v_prompt, items, max_keys, H, Hkv, M, Dh, scale,
-                                                                     part_ml, part_o);
+  if (d128)
+    prompt_attn_partial_d128_kernel<<<grid, 256, sm, as_stream(stream)>>>(
+        kv_dtype, qd, k_slab, v_slab, k_prompt, v_prompt, items, max_keys, H, Hkv, M, scale, part_ml, part_o);
+  else
+    prompt_attn_partial_kernel<<<grid, 256, sm, as_stream(stream)>>>(kv_dtype, qd, k_slab, v_slab, k_prompt,
+                                                                       v_prompt, items, max_keys, H, Hkv, M, Dh, scale,
+                                                                       part_ml, part_o);
   IFKV_LAUNCH_CHECK("prompt_attn_partial");
   return IFKV_OK;
 }
