@@ -115,7 +115,7 @@ extern "C" int ifkv_recompute_attn_tc_v10(const void* q, const void* k_layer, co
                                           int Dh, int n_rows, float scale, void* out, float* ml_out, void* stream);
 // The tcgen05 kernel (tc_recompute_attn_v10.cu): two tiles of floor(128/G)
 // tokens x G heads per CTA, P written into the TMEM columns of its own S tile
-// and read by a TS-form PV MMA part by part, a quarter of the exponentials on
+// and read by a TS-form PV MMA part by part, an eighth of the exponentials on
 // the FMA pipe, key splits below two waves.  The generations it replaced (v2,
 // v4, v5, the CTA-pair kernels v7-v9) were measured slower and moved out of
 // the library (profiles/r1_attn_ab.md, r2_attn.md, r2_attn10.md; sources in

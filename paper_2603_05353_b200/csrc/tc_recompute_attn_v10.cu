@@ -25,7 +25,7 @@
 // consumption order K0 V0 K1 V1 ...  TMEM: S_A | S_B | O_A | O_B (128 columns
 // each), P_x aliased on columns 64..127 of S_x.
 // Softmax per block: one 128-column TMEM read of S, row max, an optional O
-// rescale (O_x is idle), then each 32-key quarter's exponentials -- a quarter
+// rescale (O_x is idle), then each 32-key quarter's exponentials -- an eighth
 // of them on the FMA pipe (degree-3 polynomial), the rest on MUFU -- are
 // packed, stored over S and published, so PV_x(j) on the first keys overlaps
 // the exponentials of the later ones (profiles/r2_attn10.md: 5-15 % over the
@@ -59,9 +59,10 @@ constexpr int kSoftmaxRegs = 200, kOtherRegs = 96;  // setmaxnreg moves register
 constexpr int kParts = 4;
 constexpr int kPairs = 64 / kParts;  // column pairs (= TMEM columns of P) per part
 // FMA-pipe exponentials: in each 32-key fragment selected by FRAGS, the last
-// EMU of every 8 column pairs use the polynomial instead of MUFU (25 %)
+// EMU of every 8 column pairs use the polynomial instead of MUFU (12.5 %;
+// 0 / 25 / 37.5 / 50 % measured slower, profiles/r2_attn10.md section 5)
 #ifndef IFKV_ATTN10_EMU
-#define IFKV_ATTN10_EMU 2
+#define IFKV_ATTN10_EMU 1
 #endif
 #ifndef IFKV_ATTN10_FRAGS
 #define IFKV_ATTN10_FRAGS 0xF
