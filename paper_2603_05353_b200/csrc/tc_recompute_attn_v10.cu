@@ -56,7 +56,10 @@ constexpr int kWarpTma = 8, kWarpMma = 9, kWarpAlloc = 10;
 constexpr int kSoftmaxRegs = 200, kOtherRegs = 96;  // setmaxnreg moves registers within the CTA:
                                                      // 256 x (200 - 168) <= 128 x (168 - 96)
 // P is published in kParts parts of 128 / kParts keys as their exponentials finish
-constexpr int kParts = 4;
+#ifndef IFKV_ATTN10_PARTS
+#define IFKV_ATTN10_PARTS 4
+#endif
+constexpr int kParts = IFKV_ATTN10_PARTS;
 constexpr int kPairs = 64 / kParts;  // column pairs (= TMEM columns of P) per part
 // FMA-pipe exponentials: in each 32-key fragment selected by FRAGS, the last
 // EMU of every 8 column pairs use the polynomial instead of MUFU (12.5 %;
@@ -213,8 +216,10 @@ __device__ __forceinline__ void softmax_tile10(Smem10& sm, uint32_t tmem, int x,
       }
       if constexpr (kPairs == 32)
         tc::tmem_st32(t_p + kPairs * hf, reinterpret_cast<const float*>(p));
-      else
+      else if constexpr (kPairs == 16)
         tc::tmem_st16(t_p + kPairs * hf, p);
+      else
+        tc::tmem_st8(t_p + kPairs * hf, p);
       tc::tmem_st_wait();
       tc::tc_fence_before();
       __syncwarp();
