@@ -23,6 +23,9 @@ res = P.assemble_select_recompute(dw, store, g.chunks, g.prompt_token_ids, P.Sel
 plain = [P.prefill_chunk(dw, c) for c in g.chunks]
 res2 = P.assemble_select_recompute(dw, plain, g.chunks, g.prompt_token_ids, P.SelectionConfig(ratio=0.15))
 plan, _, _ = P.reorder_and_reselect(dw, g.chunks, g.prompt_token_ids, budget=308, prefilled=plain)
+# reorder over the store slab (first pass in place: warp-per-row merge, Dh = 128 SIMT partial)
+plan_s, _, _ = P.reorder_and_reselect(dw, g.chunks, g.prompt_token_ids, budget=308, prefilled=store)
+assert np.array_equal(plan.permutation, plan_s.permutation)
 # a larger recompute attention grid (key splits, two tiles per CTA, G = 4)
 rng = np.random.default_rng(0)
 q = torch.randn(600, 32, 128, device="cuda").bfloat16()
