@@ -154,7 +154,10 @@ extern "C" int ifkv_prompt_mm(const void* x, int P, int R, int K, const void* w,
     int rc = make_tmap_bf16(&tx, x, 2, dims, strides, box);
     if (rc) return rc;
   }
-  constexpr int kStages = 3;  // 2 CTAs per SM at P*R = 96: 6 x 16 KB of W in flight per SM
+#ifndef IFKV_PMM_STAGES
+#define IFKV_PMM_STAGES 3
+#endif
+  constexpr int kStages = IFKV_PMM_STAGES;  // 3: 2 CTAs per SM at P*R = 96, 6 x 16 KB of W in flight per SM
   const int stage_bytes = kWStage + ((NR * 128 + 1023) & ~1023);
   const size_t smem = (size_t)kStages * stage_bytes + 1024 + 2 * kStages * 8 + 8 + 16;
   auto kern = prompt_mm_kernel<kStages>;

@@ -344,6 +344,8 @@ def prompt_mm_splits(N: int, K: int, R: int, sms: int, P: int = 3) -> int:
     split partials; measured in tools/prompt_mm_bench.py), >= 2 k-steps each."""
     n_tiles, k_steps = N // 128, K // 64
     per_sm = 2 if 3 * (16384 + P * R * 128) + 2048 <= 113 * 1024 else 1  # 3-stage ring per CTA
+    if os.environ.get("IFKV_PMM_PER_SM"):  # A/B override (with a library built for another ring depth)
+        per_sm = int(os.environ["IFKV_PMM_PER_SM"])
     return max(1, min((per_sm * sms) // n_tiles, k_steps // 2))
 
 
