@@ -163,10 +163,11 @@ static int gather_launch(int dtype, int n_chunks, const void* const* src_k, cons
       int64_t w = (int64_t)chunk_len[c] * vpr * n_layers;
       if (w > max_work) max_work = w;
     }
-    // enough CTAs per chunk that all chunks together fill ~8 CTAs per SM
-    // (IFKV_GATHER_CPS: fewer, for a gather that runs beside other kernels)
-    int cps = 8;
-    if (const char* e = getenv("IFKV_GATHER_CPS")) cps = atoi(e) > 0 ? atoi(e) : 8;
+    // enough CTAs per chunk that all chunks together fill ~16 CTAs per SM
+    // (C2 in-step A/B, profiles/r2_session3/cps_ab/: 16 per SM 2.06-2.09 ms vs
+    // 8 2.25-2.63, 4 2.16-2.24, 32 2.14-2.23; IFKV_GATHER_CPS overrides)
+    int cps = 16;
+    if (const char* e = getenv("IFKV_GATHER_CPS")) cps = atoi(e) > 0 ? atoi(e) : 16;
     int64_t per_chunk = ((int64_t)sms * cps + nc - 1) / nc;
     int64_t need = (max_work + 511) / 512;
     unsigned gx = (unsigned)(need < per_chunk ? (need > 0 ? need : 1) : per_chunk);
